@@ -1,0 +1,161 @@
+"""Pins of oracle/spacetime.py: L_{tau,h}, smoother S (Eq. 2), correction A (Eq. 5)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from oracle import mesh, multigrid as mg, spacetime as st, time_dg
+
+
+def level(n=(2, 2, 2), S=4, q=1, lam=1.0, seed=0):
+    m = mesh.unit_mesh(n)
+    rng = np.random.default_rng(seed)
+    s = rng.uniform(0.5, 2, m.n_cells); nu = rng.uniform(0.5, 2, m.n_cells)
+    h = 1.0 / n[0]
+    tau = lam * h * h * rng.uniform(0.5, 1.5, S)
+    return st.Level(m, s, nu, tau, q)
+
+
+EXACT = mg.Options(inner="exact")
+
+
+def rand(lv, seed=1):
+    return np.random.default_rng(seed).uniform(-1, 1, (lv.S, lv.q + 1, lv.n))
+
+
+def test_scalar_bidiagonal_example():
+    # M = I (1x1), K = 0, q = 0: L (a, b) = (a, b - a)   (block structure of l.53-58)
+    lv = level((1, 1), S=2, q=0)
+    lv.M = sp.identity(lv.n, format="csr"); lv.K = sp.csr_matrix((lv.n, lv.n))
+    X = np.zeros((2, 1, lv.n)); X[0] = 3.0; X[1] = 5.0
+    Y = st.apply_L(lv, X)
+    assert np.all(Y[0] == 3.0) and np.all(Y[1] == 2.0)
+
+
+@pytest.mark.parametrize("q", [0, 1])
+@pytest.mark.parametrize("n", [(2, 2, 2), (3, 4)])
+def test_forward_substitution_matches_dense_direct_solve(q, n):
+    # the space-time system (l.51-77) solved (a) by a sparse direct factorisation of the whole
+    # block matrix and (b) by time stepping; both must agree and reproduce F
+    lv = level(n, S=5, q=q)
+    F = rand(lv)
+    Lfull = mg.assemble_L(lv)
+    # the dense solve orders unknowns [slab][a][edge], which is F's C order
+    Xd = spla.spsolve(Lfull.tocsc(), F.ravel()).reshape(F.shape)
+    Xf = st.forward_solve(lv, F)
+    np.testing.assert_allclose(Xf, Xd, rtol=1e-10, atol=1e-12 * np.abs(Xd).max())
+    np.testing.assert_allclose(st.apply_L(lv, Xf), F, atol=1e-10)
+    np.testing.assert_allclose(Lfull @ Xf.ravel(), st.apply_L(lv, Xf).ravel(), atol=1e-12)
+
+
+def test_sigma_t_is_prefix_sum_for_dg0():
+    # (Sigma_t y)_i = sum_{j<=i} y_j (l.182-184): blocks (1),(2),(3) -> (1),(3),(6)
+    lv = level((1, 1), S=3, q=0)
+    Z = np.zeros((3, 1, lv.nn)); Z[0] = 1; Z[1] = 2; Z[2] = 3
+    Y = st.sigma_t(lv, Z)
+    assert Y[:, 0, 0].tolist() == [1.0, 3.0, 6.0]
+
+
+@pytest.mark.parametrize("q", [0, 1])
+def test_sigma_t_inverts_time_factor(q):
+    # G^T L G = L_t (x) K_n; Sigma_t must invert L_t (backward difference for q = 0)
+    lv = level(S=6, q=q)
+    Z = np.random.default_rng(5).normal(size=(6, q + 1, lv.nn))
+    Y = st.sigma_t(lv, Z)
+    Ct, Mt, Nt = lv.Ct, lv.Mt, lv.Nt
+    back = np.einsum("ba,kan->kbn", Ct, Y)
+    back[1:] -= np.einsum("ba,kan->kbn", Nt, Y[:-1])
+    np.testing.assert_allclose(back, Z, atol=1e-13)
+
+
+@pytest.mark.parametrize("q", [0, 1])
+@pytest.mark.parametrize("n", [(2, 2, 2), (4, 4)])
+def test_correction_annihilates_gradient_residual(q, n):
+    # with exact K_n^{-1}, Eq. (5) is the Galerkin correction on range(G):
+    # G^T (f - L x_new) = 0 for ANY x, f (the nodal part dx/dt = f_n is integrated exactly, l.158-163)
+    lv = level(n, S=5, q=q)
+    for seed in range(3):
+        X = rand(lv, 10 + seed); F = rand(lv, 20 + seed)
+        before = lv.spatial(lv.G.T.tocsr(), F - st.apply_L(lv, X))
+        Xn = st.correction_A(lv, X, F, EXACT)
+        after = lv.spatial(lv.G.T.tocsr(), F - st.apply_L(lv, Xn))
+        assert np.linalg.norm(after) <= 1e-10 * np.linalg.norm(before)
+
+
+@pytest.mark.parametrize("q", [0, 1])
+def test_correction_removes_pure_gradient_error(q):
+    # f = L(G y) for nodal y, x = 0: one A leaves zero residual (the error was a pure gradient)
+    lv = level((2, 2, 2), S=4, q=q)
+    Y = np.random.default_rng(2).normal(size=(4, q + 1, lv.nn))
+    F = st.apply_L(lv, lv.spatial(lv.G, Y))
+    X = st.correction_A(lv, np.zeros_like(F), F, EXACT)
+    assert np.linalg.norm(F - st.apply_L(lv, X)) <= 1e-10 * np.linalg.norm(F)
+
+
+def test_correction_ignores_solenoidal_residual():
+    lv = level((2, 2, 2), S=3, q=1)
+    R = rand(lv)
+    # project each block onto ker(G^T) (solenoidal residual) with a dense least-squares projection
+    G = lv.G.toarray()
+    Pr = np.eye(lv.n) - G @ np.linalg.pinv(G)
+    Rs = np.einsum("ij,kaj->kai", Pr, R)
+    X0 = rand(lv, 4)
+    F = st.apply_L(lv, X0) + Rs
+    np.testing.assert_allclose(st.correction_A(lv, X0, F, EXACT), X0, atol=1e-12)
+
+
+@pytest.mark.parametrize("inner", ["exact", "jacobi"])
+def test_fixed_point(inner):
+    lv = level(S=4)
+    X = rand(lv); F = st.apply_L(lv, X)
+    o = mg.Options(inner=inner)
+    np.testing.assert_allclose(st.smoother_S(lv, X, F, o), X, atol=1e-12)
+    np.testing.assert_allclose(st.correction_A(lv, X, F, o), X, atol=1e-12)
+
+
+def test_smoother_without_time_coupling_is_damped_jacobi():
+    # S = 1 slab, exact A^{-1}: e -> (1 - omega) e (Eq. 2 with omega = 0.5)
+    lv = level(S=1)
+    Xs = rand(lv); F = st.apply_L(lv, Xs)
+    X0 = rand(lv, 9)
+    X1 = st.smoother_S(lv, X0, F, EXACT)
+    np.testing.assert_allclose(X1 - Xs, 0.5 * (X0 - Xs), atol=1e-12)
+
+
+def test_block_jacobi_sweeps_converge_to_inverse():
+    # the inner sweep z <- z + w D^{-1}(r - A z) is a consistent iteration for A_k: many sweeps -> A_k^{-1} r
+    lv = level((3, 3, 3), S=1, q=1, lam=0.2)
+    R = rand(lv)[0]
+    z = st.block_jacobi_inverse(lv, 0, R, 400, 0.6)
+    ze = lv.Ainv_exact(0).solve(R.reshape(-1)).reshape(R.shape)
+    np.testing.assert_allclose(z, ze, rtol=1e-8, atol=1e-10 * np.abs(ze).max())
+
+
+def test_nodal_jacobi_sweeps_converge_on_range():
+    lv = level((3, 3, 3), S=1, q=0)
+    W = lv.spatial(lv.G.T.tocsr(), rand(lv))
+    o = mg.Options(nu_n=3000, omega_n=0.6)
+    Z = st.Kn_inverse(lv, W, o)
+    np.testing.assert_allclose(lv.spatial(lv.Kn, Z), W, atol=1e-9 * np.abs(W).max())
+
+
+def test_hybrid_order_right_to_left():
+    # "SA is one application of A followed by an application of S" (l.208); post uses the reverse
+    lv = level(S=4)
+    X = rand(lv); F = rand(lv, 3)
+    o = mg.Options(spec="SA")
+    pre = st.hybrid_smooth(lv, X, F, o, "pre")
+    np.testing.assert_array_equal(pre, st.smoother_S(lv, st.correction_A(lv, X, F, o), F, o))
+    post = st.hybrid_smooth(lv, X, F, o, "post")
+    np.testing.assert_array_equal(post, st.correction_A(lv, st.smoother_S(lv, X, F, o), F, o))
+
+
+def test_smoothers_are_affine():
+    lv = level(S=3)
+    o = mg.Options()
+    X1, X2, F1, F2 = rand(lv, 1), rand(lv, 2), rand(lv, 3), rand(lv, 4)
+    Z = np.zeros_like(X1)
+    for op in (st.smoother_S, st.correction_A):
+        lhs = op(lv, X1 + X2, F1 + F2, o)
+        rhs = op(lv, X1, F1, o) + op(lv, X2, F2, o) - op(lv, Z, Z, o)
+        np.testing.assert_allclose(lhs, rhs, atol=1e-12)
