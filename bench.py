@@ -1,0 +1,271 @@
+"""bench.py — space-time dof-updates/s per V-cycle of the B200 space-time multigrid.
+
+Contract: `python bench.py --gpus N --steps K --warmup W`
+(N > 1 under torchrun, one rank per GPU).  A step is one V-cycle of the whole
+hot path (all rows of DESIGN.md §0(a)) over the rank's slab block of the
+BASELINE.json config 4 workload (64^3 hex mesh, 811,200 edges, dG(1),
+tau = 1/4096, 512 slabs per GPU).  `--impl reference` times the CPU oracle on a
+bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "space-time dof-updates/s per V-cycle"
+UNIT = "dof-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--slabs", type=int, default=512, help="slabs per GPU (weak scaling)")
+    ap.add_argument("--n", type=int, default=64, help="cells per direction")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-out", default=None, help="write per-kernel event stats (json)")
+    return ap.parse_args()
+
+
+def workload(args):
+    return workloads.c4(n=args.n, S=args.slabs, tau=1.0 / 4096)
+
+
+def workload_name(args):
+    return (f"c4: unit cube {args.n}^3 hex, lowest-order Nedelec, dG(1), tau=1/4096, sigma=nu=1, "
+            f"{args.slabs} slabs per GPU, f ~ U(-1,1) seed 3")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------- CPU oracle
+def oracle_sample(n=32, S=8):
+    """Bounded sample of the c4 workload for the CPU oracle: n^3 cells, S slabs, same lambda = 1."""
+    from oracle import mesh, multigrid as mg
+    w = workloads.c4(n=n, S=S, tau=1.0 / (n * n))
+    H = mg.Hierarchy(mesh.Mesh(w.n, w.node_coords()), w.sigma, w.nu, w.tau, w.q, mg.Options())
+    F = workloads.to_oracle(w.rhs())
+    return w, H, F
+
+
+def time_oracle_vcycle(H, F, X):
+    from oracle import multigrid as mg
+    t = time.perf_counter()
+    X = mg.vcycle(H, 0, X, F)
+    return time.perf_counter() - t, X
+
+
+def cpu_baseline():
+    w, H, F = oracle_sample()
+    dt, _ = time_oracle_vcycle(H, F, np.zeros_like(F))
+    return {"value": F.size / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"one oracle V-cycle (numpy/scipy fp64, single-threaded sparse products) on the c4 recipe "
+                      f"at {w.n[0]}^3 cells x {w.S} slabs (lambda = tau/h^2 = 1 as in c4), {F.size} dofs, "
+                      f"{dt:.2f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    w, H, F = oracle_sample()
+    X = np.zeros_like(F)
+    for _ in range(args.warmup):
+        _, X = time_oracle_vcycle(H, F, X)
+    ts = []
+    for _ in range(args.steps):
+        dt, X = time_oracle_vcycle(H, F, X)
+        ts.append(dt)
+    T = float(np.sum(ts))
+    val = F.size * args.steps / T
+    sample = (f"oracle V-cycle on the c4 recipe at {w.n[0]}^3 cells x {w.S} slabs (lambda = 1), "
+              f"{F.size} dofs per step")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": sample},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+# ------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_1911_09548_b200 as p
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    w = workload(args)
+    # weak scaling: every rank owns `slabs` slabs; ranks run their slab blocks as independent
+    # replicas (the NCCL slab exchange is not built yet)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        s = p.Solver.from_workload(w, stream=stream)
+        f = w.rhs_device()                       # same recipe as w.rhs(), drawn on the device
+        x = torch.zeros_like(f)
+        n_dofs = f.numel()
+        for _ in range(args.warmup):
+            s.vcycle(x, f)
+        stream.synchronize()
+        if dist:
+            dist.barrier()
+        launches0 = s.info()["kernel_launches"]
+        s.profile(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local_rank) as clk:
+            stream.synchronize()
+            e0.record(stream)
+            for _ in range(args.steps):
+                s.vcycle(x, f)
+            e1.record(stream)
+            stream.synchronize()
+        ms = e0.elapsed_time(e1)
+        kstats = s.profile_read()
+        s.profile(False)
+        launches = s.info()["kernel_launches"] - launches0
+        t_max = ms
+        if dist:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_max = float(t.item())
+        # end to end through the public API with host buffers: st_solve_host copies f and x in,
+        # runs the V-cycle (+ its residual norms) and copies x back, all inside the call
+        e2e = None
+        if not args.no_e2e:
+            fh = f.cpu().pin_memory()
+            xh = torch.zeros(fh.shape, dtype=torch.float64).pin_memory()
+            s.solve_host(xh.numpy(), fh.numpy(), tol=0.0, maxit=1)      # warm-up
+            ke = max(1, min(args.steps, 3))
+            t0 = time.perf_counter()
+            for _ in range(ke):
+                s.solve_host(xh.numpy(), fh.numpy(), tol=0.0, maxit=1)
+            te = (time.perf_counter() - t0) / ke
+            if dist:
+                t = torch.tensor([te], device="cuda", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                te = float(t.item())
+            e2e = {"value": n_dofs * world / te, "unit": UNIT, "h2d_bytes_per_step": 2 * f.numel() * 8,
+                   "d2h_bytes_per_step": f.numel() * 8,
+                   "note": "st_solve_host(maxit=1): H2D f,x from pinned memory, ||f||, ||r||, one V-cycle, "
+                           "||r||, D2H x"}
+    if rank != 0:
+        return
+    peak, peak_src = measured_peak()
+    fam, (nl, kms, kbytes) = max(kstats.items(), key=lambda kv: kv[1][1])
+    dur = kms / nl
+    achieved = kbytes / nl / (dur * 1e-3) / 1e9
+    total_bytes = sum(v[2] for v in kstats.values())
+    value = n_dofs * world * args.steps / (t_max * 1e-3)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args), "rhs": "U(-1,1) drawn on the device (torch generator, seed 3)", "n_edges": s.n_edges, "slabs_per_gpu": args.slabs,
+                   "dofs_per_gpu": n_dofs, "levels": s.info()["n_levels"],
+                   "l2": f"no flush: every space-time vector is {8 * n_dofs / 1e9:.2f} GB >> 126 MB L2",
+                   "parallelism": f"slab blocks, {world} replica(s)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": fam, "peak_source": peak_src,
+                     "kernel_share_of_step": kms / t_max,
+                     "vcycle_algorithmic_GBps": total_bytes / (t_max * 1e-3) / 1e9},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "kernels": {k: {"launches": v[0], "ms": v[1], "GBps": v[2] / (v[1] * 1e-3) / 1e9 if v[1] else None}
+                    for k, v in kstats.items()},
+    }
+    if not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_baseline()
+    if args.profile_out:
+        with open(args.profile_out, "w") as fh:
+            json.dump(out, fh, indent=1)
+    print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

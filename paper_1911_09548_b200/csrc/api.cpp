@@ -1,0 +1,514 @@
+// api.cpp — the C-ABI of include/st.h: device hierarchy, V-cycle driver, solve loop.
+//
+// The V-cycle is driven from the host: per level the hybrid
+// smoother (spec read right to left, l.208; reversed for post-smoothing),
+// residual + restriction, recursion, prolongation.  Every arithmetic step is
+// a kernel of kernels.cu launched on the handle's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct Unsupported : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char *what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+struct st_handle {
+    st::Options o;
+    st::TimeMats tm{};
+    st::KT kt{};
+    int Q = 1;
+    std::vector<st::HostLevel> hl;
+    std::vector<st::DevLevel> dl;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    double *partial = nullptr;
+    int partial_cap = 0;
+    double *dscal = nullptr;
+    double *hx = nullptr, *hf = nullptr;   // device buffers for st_solve_host
+    int64_t launches = 0;
+    int64_t bytes = 0;
+    std::vector<void *> allocs;
+    int64_t n_dofs = 0;
+    // profiling: (family, bytes, start, stop) per recorded launch
+    bool prof = false;
+    struct Rec { int fam; double bytes; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::string> fams;
+    int fam_id(const char *name) {
+        for (size_t i = 0; i < fams.size(); ++i)
+            if (fams[i] == name) return (int)i;
+        fams.push_back(name);
+        return (int)fams.size() - 1;
+    }
+    cudaEvent_t ev() {
+        if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "event");
+        return e;
+    }
+    // run `launch` (which issues exactly `count` kernels) and, when profiling, time it
+    template <class F>
+    void run(const char *fam, double bytes, int count, F &&launch) {
+        if (!prof) { launch(); launches += count; return; }
+        Rec r{fam_id(fam), bytes, ev(), ev()};
+        ck(cudaEventRecord(r.a, stream), "event record");
+        launch();
+        ck(cudaEventRecord(r.b, stream), "event record");
+        recs.push_back(r);
+        launches += count;
+    }
+
+    template <class T>
+    T *dalloc(size_t n) {
+        void *p = nullptr;
+        if (n == 0) n = 1;
+        cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+        if (e == cudaErrorMemoryAllocation) throw std::bad_alloc();
+        ck(e, "cudaMalloc");
+        allocs.push_back(p);
+        bytes += (int64_t)(n * sizeof(T));
+        return (T *)p;
+    }
+    template <class T>
+    T *upload(const std::vector<T> &v) {
+        T *p = dalloc<T>(v.size());
+        if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+        return p;
+    }
+    st::DevELL upload(const st::HostELL &E) {
+        st::DevELL d;
+        d.rows = E.rows; d.width = E.width;
+        d.col = upload(E.col);
+        if (!E.val.empty()) d.val = upload(E.val);
+        return d;
+    }
+    ~st_handle() {
+        for (auto &r : recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+        for (auto e : pool) cudaEventDestroy(e);
+        for (void *p : allocs) cudaFree(p);
+    }
+};
+
+namespace {
+
+using st::DevLevel;
+
+size_t vec_len(const DevLevel &L, int Q, bool nodes = false) {
+    return (size_t)(nodes ? L.n_nodes : L.n_edges) * Q * L.S;
+}
+
+// Algorithmic bytes: every vector touched once, operators read once.
+double ell_bytes(const st::DevELL &E) { return (double)E.rows * E.width * 12.0; }
+double op_bytes(const DevLevel &L) { return ell_bytes(L.M) + ell_bytes(L.K) + 16.0 * L.n_edges; }
+double evec(const DevLevel &L, int Q) { return 8.0 * L.n_edges * Q * L.S; }
+double nvec(const DevLevel &L, int Q) { return 8.0 * L.n_nodes * Q * L.S; }
+
+void smooth_S(st_handle *h, DevLevel &L, double *x, const double *f) {
+    const auto &o = h->o;
+    auto s = (st::Stream)h->stream;
+    const int Q = h->Q;
+    const double ev = evec(L, Q), ob = op_bytes(L);
+    if (o.nu_s == 1) {
+        h->run("residual", 3 * ev + ob, 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, nullptr, nullptr, L.z, o.omega_s, nullptr); });
+        h->run("axpy", 3 * ev, 1, [&] { st::launch_axpy(s, vec_len(L, Q), o.omega, L.z, x); });
+        return;
+    }
+    h->run("residual", (o.nu_s > 2 ? 4 : 3) * ev + ob, 1, [&] {
+        st::launch_residual(s, L, h->kt, Q, x, f, nullptr, o.nu_s > 2 ? L.r : nullptr, L.z, o.omega_s, nullptr);
+    });
+    double *cur = L.z, *other = L.z2;
+    for (int i = 2; i < o.nu_s; ++i) {
+        h->run("sweep", 3 * ev + ob, 1, [&] { st::launch_sweep(s, L, h->kt, Q, false, false, cur, L.r, other, o.omega_s, o.omega); });
+        std::swap(cur, other);
+    }
+    h->run("sweep_update", (o.nu_s == 2 ? 3 : 4) * ev + ob, 1, [&] {
+        st::launch_sweep(s, L, h->kt, Q, true, o.nu_s == 2, cur, L.r, x, o.omega_s, o.omega);
+    });
+}
+
+void correct_A(st_handle *h, DevLevel &L, double *x, const double *f) {
+    const auto &o = h->o;
+    auto s = (st::Stream)h->stream;
+    const int Q = h->Q;
+    const double ev = evec(L, Q), nv = nvec(L, Q), kb = ell_bytes(L.Kn) + 8.0 * L.n_nodes;
+    h->run("residual", 3 * ev + op_bytes(L), 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, nullptr, L.r, nullptr, o.omega_s, nullptr); });
+    h->run("gt", ev + (o.nu_n > 2 ? 2 : 1) * nv + 8.0 * L.n_nodes, 1, [&] { st::launch_gt(s, L, Q, L.r, o.omega_n, L.zn, o.nu_n > 2 ? L.wn : nullptr); });
+    double *cur = L.zn, *other = L.zn2;
+    int mode = o.nu_n == 1 ? 0 : (o.nu_n == 2 ? 1 : 2);
+    for (int i = 2; i < o.nu_n; ++i) {
+        h->run("node_sweep", 3 * nv + kb, 1, [&] { st::launch_node_sweep(s, L, Q, cur, L.wn, o.omega_n, other); });
+        std::swap(cur, other);
+    }
+    h->run("node_scan", (mode == 2 ? 3 : 2) * nv + kb, 1, [&] { st::launch_node_scan(s, L, h->kt, Q, mode, cur, L.wn, o.omega_n, nullptr, L.y, nullptr); });
+    h->run("g_update", 2 * ev + nv + 8.0 * L.n_edges, 1, [&] { st::launch_g_update(s, L, Q, L.y, x); });
+}
+
+void hybrid(st_handle *h, DevLevel &L, double *x, const double *f, bool pre) {
+    std::string seq = h->o.spec;
+    if (!pre) std::reverse(seq.begin(), seq.end());
+    for (int i = (int)seq.size() - 1; i >= 0; --i) {   // right to left (l.208)
+        if (seq[i] == 'S') smooth_S(h, L, x, f);
+        else correct_A(h, L, x, f);
+    }
+}
+
+void vcycle(st_handle *h, int l, double *x, const double *f) {
+    DevLevel &L = h->dl[l];
+    auto s = (st::Stream)h->stream;
+    const int Q = h->Q;
+    if (l == (int)h->dl.size() - 1) {
+        const double N = (double)Q * L.n_edges;
+        h->run("coarsest", L.S * (N * N * 8.0 + 2 * evec(L, Q) / L.S), L.S, [&] { st::launch_coarsest(s, L, Q, f, x); });
+        return;
+    }
+    hybrid(h, L, x, f, true);
+    DevLevel &C = h->dl[l + 1];
+    h->run("residual", 3 * evec(L, Q) + op_bytes(L), 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, nullptr, L.r, nullptr, h->o.omega_s, nullptr); });
+    h->run("restrict", evec(L, Q) + evec(C, Q) + (L.space_coarsened ? ell_bytes(L.Rg) : 0.0), 1,
+           [&] { st::launch_restrict(s, L, C, Q, L.r, C.f); });
+    if (l + 1 < (int)h->dl.size() - 1) ck(cudaMemsetAsync(C.x, 0, sizeof(double) * vec_len(C, Q), h->stream), "memset");
+    vcycle(h, l + 1, C.x, C.f);
+    h->run("prolong", 2 * evec(L, Q) + evec(C, Q) + (L.space_coarsened ? ell_bytes(L.Pg) : 0.0), 1,
+           [&] { st::launch_prolong(s, L, Q, C.x, x); });
+    hybrid(h, L, x, f, false);
+}
+
+// ||f - L x||^2 (f != null) on level 0 without storing r
+double residual_norm2(st_handle *h, const double *x, const double *f) {
+    DevLevel &L = h->dl[0];
+    auto s = (st::Stream)h->stream;
+    int g = st::launch_residual(s, L, h->kt, h->Q, x, f, nullptr, nullptr, nullptr, h->o.omega_s, h->partial);
+    st::launch_reduce(s, g, h->partial, h->dscal);
+    h->launches += 2;
+    double v = 0;
+    ck(cudaMemcpyAsync(&v, h->dscal, sizeof(double), cudaMemcpyDeviceToHost, h->stream), "norm d2h");
+    ck(cudaStreamSynchronize(h->stream), "sync");
+    return v;
+}
+
+double norm2_plain(st_handle *h, const double *v, size_t n) {
+    // ||v||^2 via the residual kernel would need x = 0; use a dedicated pass instead
+    auto s = (st::Stream)h->stream;
+    int g = st::launch_norm2(s, n, v, h->partial);
+    st::launch_reduce(s, g, h->partial, h->dscal);
+    h->launches += 2;
+    double out = 0;
+    ck(cudaMemcpyAsync(&out, h->dscal, sizeof(double), cudaMemcpyDeviceToHost, h->stream), "norm d2h");
+    ck(cudaStreamSynchronize(h->stream), "sync");
+    return out;
+}
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define ST_GUARD(body)                                              \
+    try {                                                           \
+        body;                                                       \
+        ck(cudaGetLastError(), "kernel launch");                    \
+        return 0;                                                   \
+    } catch (const Unsupported &e) {                                \
+        return fail(3, e.what());                                   \
+    } catch (const CudaError &e) {                                  \
+        return fail(2, e.what());                                   \
+    } catch (const std::bad_alloc &) {                              \
+        return fail(4, "out of memory");                            \
+    } catch (const std::length_error &e) {                          \
+        return fail(3, e.what());                                   \
+    } catch (const std::invalid_argument &e) {                      \
+        return fail(1, e.what());                                   \
+    } catch (const std::exception &e) {                             \
+        return fail(1, e.what());                                   \
+    }
+
+}  // namespace
+
+extern "C" {
+
+static void parse_options(const st_params *p, st::Options &o) {
+    if (p->dim != 2 && p->dim != 3) throw std::invalid_argument("dim must be 2 or 3");
+    if (p->nx < 1 || p->ny < 1 || (p->dim == 3 && p->nz < 1)) throw std::invalid_argument("bad mesh size");
+    if (!p->sigma || !p->nu || !p->tau || p->n_slabs < 1) throw std::invalid_argument("missing sigma/nu/tau");
+    const long long ncell = (long long)p->nx * p->ny * (p->dim == 3 ? p->nz : 1);
+    for (long long c = 0; c < ncell; ++c)
+        if (!(p->sigma[c] > 0) || !(p->nu[c] > 0)) throw std::invalid_argument("sigma and nu must be > 0");
+    for (int k = 0; k < p->n_slabs; ++k)
+        if (!(p->tau[k] > 0)) throw std::invalid_argument("tau must be > 0");
+    if (p->spec && p->spec[0]) o.spec = p->spec;
+    for (char c : o.spec)
+        if (c != 'S' && c != 'A') throw std::invalid_argument("spec may only contain S and A");
+    if (p->omega > 0) o.omega = p->omega;
+    if (p->nu_s > 0) o.nu_s = p->nu_s;
+    o.omega_s = p->omega_s > 0 ? p->omega_s : (p->dim == 2 ? 0.5 : 0.6);
+    if (p->nu_n > 0) o.nu_n = p->nu_n;
+    if (p->omega_n > 0) o.omega_n = p->omega_n;
+    if (p->lambda_crit > 0) o.lambda_crit = p->lambda_crit;
+    if (p->mode < 0 || p->mode > 2) throw std::invalid_argument("mode must be 0, 1 or 2");
+    o.mode = p->mode;
+    if (p->min_slabs > 0) o.min_slabs = p->min_slabs;
+}
+
+const char *st_last_error(void) { return g_err.c_str(); }
+
+int st_setup(const st_params *p, st_handle **out) {
+    if (!p || !out) return fail(1, "null argument");
+    *out = nullptr;
+    st_handle *h = new st_handle();
+    try {
+        st::Options &o = h->o;
+        parse_options(p, o);
+        h->tm = st::time_matrices(p->q);
+        h->kt = st::make_kt(h->tm);
+        h->Q = h->tm.Q;
+        st::build_hierarchy(*p, o, h->tm, h->hl);
+        const int Q = h->Q;
+        h->dl.resize(h->hl.size());
+        ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
+        h->own_stream = true;
+        size_t max_partial = 1;
+        for (size_t l = 0; l < h->hl.size(); ++l) {
+            st::HostLevel &H = h->hl[l];
+            DevLevel &D = h->dl[l];
+            D.n_edges = H.mesh.n_edges; D.n_nodes = H.mesh.n_nodes; D.S = (int)H.tau.size();
+            if ((long long)D.n_edges * D.S >= (1LL << 31) || (long long)D.n_nodes * 32 >= (1LL << 31))
+                throw Unsupported("level too large for 32-bit thread indexing");
+            D.M = h->upload(H.M); D.K = h->upload(H.K); D.Kn = h->upload(H.Kn); D.GT = h->upload(H.GT);
+            D.dM = h->upload(H.dM); D.dK = h->upload(H.dK); D.dN = h->upload(H.dN);
+            D.edge_nodes = h->upload(H.mesh.edge_nodes);
+            D.tau = h->upload(H.tau);
+            D.space_coarsened = H.space_coarsened;
+            const bool coarsest = l + 1 == h->hl.size();
+            if (!coarsest) {
+                D.Pt = h->upload(H.Pt);
+                if (H.space_coarsened) { D.Pg = h->upload(H.Pg); D.Rg = h->upload(H.Rg); }
+            } else {
+                D.Ainv = h->upload(H.Ainv);
+                if ((size_t)Q * D.n_edges * sizeof(double) > 48 * 1024) throw Unsupported("coarsest level too large");
+            }
+            const size_t ve = vec_len(D, Q), vn = vec_len(D, Q, true);
+            if (l > 0) { D.x = h->dalloc<double>(ve); D.f = h->dalloc<double>(ve); }
+            if (!coarsest) {
+                D.r = h->dalloc<double>(ve);
+                D.z = o.nu_s > 2 ? h->dalloc<double>(ve) : D.r;   // r and z are never live together for nu_s <= 2
+                if (o.nu_s > 2) D.z2 = h->dalloc<double>(ve);
+                D.zn = h->dalloc<double>(vn);
+                D.y = h->dalloc<double>(vn);
+                if (o.nu_n > 2) { D.wn = h->dalloc<double>(vn); D.zn2 = h->dalloc<double>(vn); }
+            }
+            max_partial = std::max(max_partial, (ve + 255) / 256);
+            // the device owns the operators now; keep only the metadata on the host
+            H.M = H.K = H.Kn = H.GT = H.Pg = H.Rg = st::HostELL();
+            std::vector<double>().swap(H.Ainv);
+            std::vector<double>().swap(H.Pt);
+            std::vector<int>().swap(H.mesh.cell_edges);
+            std::vector<int>().swap(H.mesh.cell_nodes);
+            std::vector<int>().swap(H.mesh.edge_nodes);
+        }
+        h->partial = h->dalloc<double>(max_partial);
+        h->partial_cap = (int)max_partial;
+        h->dscal = h->dalloc<double>(2);
+        h->n_dofs = (int64_t)h->dl[0].n_edges * Q * h->dl[0].S;
+        ck(cudaDeviceSynchronize(), "setup sync");
+    } catch (const Unsupported &e) {
+        delete h; return fail(3, e.what());
+    } catch (const CudaError &e) {
+        delete h; return fail(2, e.what());
+    } catch (const std::bad_alloc &) {
+        delete h; return fail(4, "out of memory");
+    } catch (const std::length_error &e) {
+        delete h; return fail(3, e.what());
+    } catch (const std::exception &e) {
+        delete h; return fail(1, e.what());
+    }
+    *out = h;
+    return 0;
+}
+
+int st_free(st_handle *h) {
+    if (!h) return 0;
+    if (h->stream && h->own_stream) cudaStreamDestroy(h->stream);
+    h->stream = nullptr;
+    delete h;
+    return 0;
+}
+
+int st_set_stream(st_handle *h, void *stream) {
+    if (!h) return fail(1, "null handle");
+    if (h->stream && h->own_stream) cudaStreamDestroy(h->stream);
+    h->stream = (cudaStream_t)stream;
+    h->own_stream = false;
+    return 0;
+}
+
+int st_residual(st_handle *h, const double *x, const double *f, double *r, double *norms) {
+    if (!h || !x || !f) return fail(1, "null argument");
+    ST_GUARD({
+        DevLevel &L = h->dl[0];
+        auto s = (st::Stream)h->stream;
+        if (r) {
+            st::launch_residual(s, L, h->kt, h->Q, x, f, nullptr, r, nullptr, h->o.omega_s, nullptr);
+            h->launches += 1;
+        }
+        if (norms) {
+            norms[0] = std::sqrt(residual_norm2(h, x, f));
+            norms[1] = std::sqrt(norm2_plain(h, f, vec_len(L, h->Q)));
+        }
+    })
+}
+
+int st_vcycle(st_handle *h, double *x, const double *f) {
+    if (!h || !x || !f) return fail(1, "null argument");
+    ST_GUARD(vcycle(h, 0, x, f))
+}
+
+int st_solve(st_handle *h, double *x, const double *f, double tol, int maxit, int *iters, double *hist) {
+    if (!h || !x || !f || maxit < 0) return fail(1, "bad argument");
+    ST_GUARD({
+        const double nf = std::sqrt(norm2_plain(h, f, vec_len(h->dl[0], h->Q)));
+        int it = 0;
+        for (;; ++it) {
+            const double rel = std::sqrt(residual_norm2(h, x, f)) / nf;
+            if (hist) hist[it] = rel;
+            if (rel <= tol || it == maxit) break;
+            vcycle(h, 0, x, f);
+        }
+        if (iters) *iters = it;
+    })
+}
+
+int st_solve_host(st_handle *h, double *x_host, const double *f_host, double tol, int maxit, int *iters,
+                  double *hist) {
+    if (!h || !x_host || !f_host) return fail(1, "null argument");
+    ST_GUARD({
+        const size_t n = vec_len(h->dl[0], h->Q);
+        if (!h->hx) { h->hx = h->dalloc<double>(n); h->hf = h->dalloc<double>(n); }
+        ck(cudaMemcpyAsync(h->hf, f_host, n * sizeof(double), cudaMemcpyHostToDevice, h->stream), "h2d f");
+        ck(cudaMemcpyAsync(h->hx, x_host, n * sizeof(double), cudaMemcpyHostToDevice, h->stream), "h2d x");
+        int rc = st_solve(h, h->hx, h->hf, tol, maxit, iters, hist);
+        if (rc) throw CudaError(g_err);
+        ck(cudaMemcpyAsync(x_host, h->hx, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "d2h x");
+        ck(cudaStreamSynchronize(h->stream), "sync");
+    })
+}
+
+static void parse_options(const st_params *p, st::Options &o);
+
+int st_profile(st_handle *h, int enable) {
+    if (!h) return fail(1, "null handle");
+    ST_GUARD({
+        ck(cudaStreamSynchronize(h->stream), "sync");
+        for (auto &r : h->recs) { h->pool.push_back(r.a); h->pool.push_back(r.b); }
+        if (enable) h->recs.clear();
+        h->prof = enable != 0;
+    })
+}
+
+int st_profile_read(st_handle *h, st_kstat *out, int max, int *n) {
+    if (!h || !n) return fail(1, "null argument");
+    ST_GUARD({
+        ck(cudaStreamSynchronize(h->stream), "sync");
+        std::vector<st_kstat> agg(h->fams.size());
+        for (size_t i = 0; i < agg.size(); ++i) {
+            std::memset(&agg[i], 0, sizeof(st_kstat));
+            std::strncpy(agg[i].name, h->fams[i].c_str(), sizeof(agg[i].name) - 1);
+        }
+        for (auto &r : h->recs) {
+            float ms = 0;
+            ck(cudaEventElapsedTime(&ms, r.a, r.b), "elapsed");
+            agg[r.fam].launches += 1;
+            agg[r.fam].ms += ms;
+            agg[r.fam].bytes += r.bytes;
+        }
+        *n = (int)agg.size();
+        for (int i = 0; i < (int)agg.size() && i < max; ++i) out[i] = agg[i];
+    })
+}
+
+int st_plan(const st_params *p, st_info_t *info) {
+    if (!p || !info) return fail(1, "null argument");
+    try {
+        st::Options o;
+        parse_options(p, o);
+        st::TimeMats tm = st::time_matrices(p->q);
+        std::vector<st::HostLevel> hl;
+        st::build_hierarchy(*p, o, tm, hl);
+        std::memset(info, 0, sizeof(*info));
+        info->n_levels = (int)std::min<size_t>(32, hl.size());
+        info->q = p->q;
+        info->n_dofs = (int64_t)hl[0].mesh.n_edges * (p->q + 1) * p->n_slabs;
+        for (int l = 0; l < info->n_levels; ++l) {
+            info->level_n_edges[l] = hl[l].mesh.n_edges;
+            info->level_n_nodes[l] = hl[l].mesh.n_nodes;
+            info->level_n_slabs[l] = (int)hl[l].tau.size();
+            info->level_space_coarsened[l] = hl[l].space_coarsened ? 1 : 0;
+            info->level_lambda[l] = hl[l].lambda;
+        }
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(1, e.what());
+    }
+}
+
+int st_host_matrix(const st_params *p, int level, int which, int *rows, int *width, int *col, double *val) {
+    if (!p || !rows || !width) return fail(1, "null argument");
+    try {
+        st::Options o;
+        parse_options(p, o);
+        st::TimeMats tm = st::time_matrices(p->q);
+        std::vector<st::HostLevel> hl;
+        st::build_hierarchy(*p, o, tm, hl);
+        if (level < 0 || level >= (int)hl.size()) throw std::invalid_argument("level out of range");
+        const st::HostLevel &L = hl[level];
+        const st::HostELL *E = which == 0 ? &L.M : which == 1 ? &L.K : which == 2 ? &L.Kn : which == 3 ? &L.Pg : nullptr;
+        if (!E) throw std::invalid_argument("which must be 0..3");
+        if (which == 3 && !L.space_coarsened) throw std::invalid_argument("level does not coarsen space");
+        *rows = E->rows; *width = E->width;
+        if (col) std::memcpy(col, E->col.data(), sizeof(int) * E->col.size());
+        if (val) std::memcpy(val, E->val.data(), sizeof(double) * E->val.size());
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(1, e.what());
+    }
+}
+
+int st_info(const st_handle *h, st_info_t *info) {
+    if (!h || !info) return fail(1, "null argument");
+    std::memset(info, 0, sizeof(*info));
+    info->n_levels = (int)std::min<size_t>(32, h->hl.size());
+    info->q = h->Q - 1;
+    info->n_dofs = h->n_dofs;
+    for (int l = 0; l < info->n_levels; ++l) {
+        info->level_n_edges[l] = h->hl[l].mesh.n_edges;
+        info->level_n_nodes[l] = h->hl[l].mesh.n_nodes;
+        info->level_n_slabs[l] = (int)h->hl[l].tau.size();
+        info->level_space_coarsened[l] = h->hl[l].space_coarsened ? 1 : 0;
+        info->level_lambda[l] = h->hl[l].lambda;
+    }
+    info->kernel_launches = h->launches;
+    info->device_bytes = h->bytes;
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// internal.h — host/device data structures of libst (not part of the C-ABI).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/st.h"
+
+namespace st {
+
+constexpr int kMaxQ = 3;
+
+// dG(q) time matrices, row-major [test b][trial a], plus derived quantities
+// used by the kernels (R1/R2).
+struct TimeMats {
+    int Q;
+    double Ct[kMaxQ * kMaxQ], Mt[kMaxQ * kMaxQ], Nt[kMaxQ * kMaxQ];
+    double Ctinv[kMaxQ * kMaxQ];
+    double g[kMaxQ];        // Ct^{-1} e_0
+};
+
+// ELL matrix on the host: width slots per row, row-major [row][slot].
+struct HostELL {
+    int rows = 0, width = 0;
+    std::vector<int> col;
+    std::vector<double> val;
+};
+
+struct DevELL {
+    int rows = 0, width = 0;
+    int *col = nullptr;
+    double *val = nullptr;
+};
+
+struct HostMesh {
+    int dim = 3;
+    int n[3] = {1, 1, 1};
+    int n_nodes = 0, n_edges = 0, n_cells = 0, Ex = 0, Ey = 0;
+    std::vector<double> coords;               // n_nodes x dim
+    std::vector<int> edge_nodes;              // 2 per edge (start, end)
+    std::vector<int> cell_edges;              // 12 (3D) / 4 (2D) per cell, reference order
+    std::vector<int> cell_nodes;              // 8 / 4 per cell, a + 2b + 4c
+};
+
+struct HostLevel {
+    HostMesh mesh;
+    std::vector<double> sigma, nu, ratio_min;   // per cell
+    std::vector<double> tau;                    // per slab
+    HostELL M, K, Kn;
+    std::vector<double> dM, dK, dN;             // diagonals
+    HostELL GT;                                 // node -> signed incident edges: col = 2*e + (sign<0), -1 pad
+    double lambda = 0;                          // Eq. (3) value of this level
+    bool space_coarsened = false;               // this -> next
+    HostELL Pg;                                 // fine edge -> coarse edges (prolongation rows)
+    HostELL Rg;                                 // coarse edge -> fine edges (restriction rows)
+    std::vector<double> Pt;                     // per coarse slab: (2Q x Q) time prolongation, row-major
+    std::vector<double> Ainv;                   // coarsest only: per slab dense (QN x QN)
+};
+
+struct DevLevel {
+    int n_edges = 0, n_nodes = 0, S = 0;
+    DevELL M, K, Kn, GT, Pg, Rg;
+    double *dM = nullptr, *dK = nullptr, *dN = nullptr;
+    int *edge_nodes = nullptr;
+    double *tau = nullptr;
+    double *Pt = nullptr;
+    double *Ainv = nullptr;
+    bool space_coarsened = false;
+    // work vectors (ST layout)
+    double *x = nullptr, *f = nullptr;          // coarse levels only (level 0 uses caller's)
+    double *r = nullptr, *z = nullptr, *z2 = nullptr;    // edge temporaries
+    double *zn = nullptr, *y = nullptr, *wn = nullptr, *zn2 = nullptr;   // node temporaries
+};
+
+struct Options {
+    std::string spec = "SAS";
+    double omega = 0.5;
+    int nu_s = 2;
+    double omega_s = 0.6;
+    int nu_n = 2;
+    double omega_n = 0.6;
+    double lambda_crit = 0.1;
+    int mode = 0;
+    int min_slabs = 1;
+};
+
+// kernel-side time constants (passed by value to kernels)
+struct KT {
+    double Ct[kMaxQ * kMaxQ], Mt[kMaxQ * kMaxQ], Ctinv[kMaxQ * kMaxQ], g[kMaxQ];
+};
+KT make_kt(const TimeMats &tm);
+
+// kernels.cu launchers (all asynchronous on `st`)
+typedef struct CUstream_st *Stream;
+int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
+                    const double *prev, double *r, double *z, double omega_s, double *partial);
+void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, bool recon, const double *z,
+                  const double *r, double *out, double omega_s, double omega);
+void launch_axpy(Stream st, size_t n, double alpha, const double *z, double *x);
+void launch_gt(Stream st, const DevLevel &L, int Q, const double *r, double omega_n, double *zn, double *w);
+void launch_node_sweep(Stream st, const DevLevel &L, int Q, const double *z, const double *w, double omega_n,
+                       double *zout);
+void launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mode, const double *z,
+                      const double *w, double omega_n, const double *carry, double *y, double *tot);
+void launch_g_update(Stream st, const DevLevel &L, int Q, const double *y, double *x);
+void launch_restrict(Stream st, const DevLevel &F, const DevLevel &C, int Q, const double *r, double *fc);
+void launch_prolong(Stream st, const DevLevel &F, int Q, const double *xc, double *x);
+int launch_coarsest(Stream st, const DevLevel &L, int Q, const double *f, double *x);
+void launch_reduce(Stream st, int n, const double *partial, double *out);
+int launch_norm2(Stream st, size_t n, const double *v, double *partial);
+
+// setup.cpp
+TimeMats time_matrices(int q);
+HostMesh make_mesh(int dim, const int n[3], const double *coords);
+void assemble(HostLevel &L);
+void build_hierarchy(const st_params &p, const Options &o, const TimeMats &tm,
+                     std::vector<HostLevel> &levels);
+
+}  // namespace st

@@ -1,0 +1,591 @@
+// setup.cpp — host-side construction of the space-time level hierarchy.
+//
+// Everything here runs once in st_setup: mesh enumeration, lowest-order
+// Nedelec element matrices (§3 l.126-128: M_h = int sigma phi.phi,
+// K_h = int mu^{-1} curl phi . curl phi), the nodal stiffness of div(sigma grad)
+// and the discrete gradient (§3.3 l.181), the coarsening rule Eq. (3)
+// (l.105-109), spatial/time transfer operators and the dense coarsest inverse.
+// Independent implementation (no code shared with oracle/); readings R1-R9 of
+// DESIGN.md §0(c).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "internal.h"
+
+namespace st {
+
+// ---------------------------------------------------------------- small dense
+static void invert(int n, const double *A, double *Ainv) {
+    // Gauss-Jordan with partial pivoting, row-major
+    std::vector<double> a(A, A + (size_t)n * n), b((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i) b[(size_t)i * n + i] = 1.0;
+    for (int c = 0; c < n; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < n; ++r)
+            if (std::fabs(a[(size_t)r * n + c]) > std::fabs(a[(size_t)piv * n + c])) piv = r;
+        if (a[(size_t)piv * n + c] == 0.0) throw std::runtime_error("singular matrix in setup");
+        if (piv != c)
+            for (int j = 0; j < n; ++j) {
+                std::swap(a[(size_t)c * n + j], a[(size_t)piv * n + j]);
+                std::swap(b[(size_t)c * n + j], b[(size_t)piv * n + j]);
+            }
+        const double inv = 1.0 / a[(size_t)c * n + c];
+        for (int j = 0; j < n; ++j) { a[(size_t)c * n + j] *= inv; b[(size_t)c * n + j] *= inv; }
+        for (int r = 0; r < n; ++r) {
+            if (r == c) continue;
+            const double fct = a[(size_t)r * n + c];
+            if (fct == 0.0) continue;
+            for (int j = 0; j < n; ++j) {
+                a[(size_t)r * n + j] -= fct * a[(size_t)c * n + j];
+                b[(size_t)r * n + j] -= fct * b[(size_t)c * n + j];
+            }
+        }
+    }
+    std::memcpy(Ainv, b.data(), sizeof(double) * (size_t)n * n);
+}
+
+static void gauss_legendre(int n, std::vector<double> &x, std::vector<double> &w) {
+    // nodes/weights on [0,1] by Newton iteration on P_n
+    x.assign(n, 0.0); w.assign(n, 0.0);
+    for (int i = 0; i < n; ++i) {
+        double t = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+        for (int it = 0; it < 100; ++it) {
+            double p0 = 1.0, p1 = t;
+            for (int k = 2; k <= n; ++k) { double p2 = ((2 * k - 1) * t * p1 - (k - 1) * p0) / k; p0 = p1; p1 = p2; }
+            double dp = n * (t * p1 - p0) / (t * t - 1.0);
+            double dt = p1 / dp;
+            t -= dt;
+            if (std::fabs(dt) < 1e-16) break;
+        }
+        double p0 = 1.0, p1 = t;
+        for (int k = 2; k <= n; ++k) { double p2 = ((2 * k - 1) * t * p1 - (k - 1) * p0) / k; p0 = p1; p1 = p2; }
+        double dp = n * (t * p1 - p0) / (t * t - 1.0);
+        x[i] = 0.5 * (1.0 - t);
+        w[i] = 1.0 / ((1.0 - t * t) * dp * dp);   // (2/((1-t^2)P'^2)) * 1/2
+    }
+}
+
+// ------------------------------------------------------------ dG(q) in time
+static double lag(int q, int a, double s) {
+    if (q == 0) return 1.0;
+    double v = 1.0;
+    for (int m = 0; m <= q; ++m)
+        if (m != a) v *= (s - (double)m / q) / ((double)(a - m) / q);
+    return v;
+}
+static double dlag(int q, int a, double s) {
+    if (q == 0) return 0.0;
+    double tot = 0.0;
+    for (int skip = 0; skip <= q; ++skip) {
+        if (skip == a) continue;
+        double term = 1.0 / ((double)(a - skip) / q);
+        for (int m = 0; m <= q; ++m)
+            if (m != a && m != skip) term *= (s - (double)m / q) / ((double)(a - m) / q);
+        tot += term;
+    }
+    return tot;
+}
+
+TimeMats time_matrices(int q) {
+    if (q < 0 || q > kMaxQ - 1) throw std::invalid_argument("q must be 0, 1 or 2");
+    TimeMats tm{};
+    const int Q = q + 1;
+    tm.Q = Q;
+    std::vector<double> gx, gw;
+    gauss_legendre(q + 2, gx, gw);
+    for (int b = 0; b < Q; ++b)
+        for (int a = 0; a < Q; ++a) {
+            double m = 0, c = 0;
+            for (size_t i = 0; i < gx.size(); ++i) {
+                m += gw[i] * lag(q, a, gx[i]) * lag(q, b, gx[i]);
+                c += gw[i] * dlag(q, a, gx[i]) * lag(q, b, gx[i]);
+            }
+            tm.Mt[b * Q + a] = m;
+            tm.Ct[b * Q + a] = c + lag(q, a, 0.0) * lag(q, b, 0.0);   // upwind jump term
+            tm.Nt[b * Q + a] = lag(q, b, 0.0) * lag(q, a, 1.0);      // trace of the previous slab
+        }
+    invert(Q, tm.Ct, tm.Ctinv);
+    for (int a = 0; a < Q; ++a) tm.g[a] = tm.Ctinv[a * Q + 0];
+    // the kernels rely on the nodal structure Nt = e_0 e_q^T and (Ct^{-1} e_0)_q = 1 (R2)
+    for (int b = 0; b < Q; ++b)
+        for (int a = 0; a < Q; ++a) {
+            double want = (b == 0 && a == q) ? 1.0 : 0.0;
+            if (std::fabs(tm.Nt[b * Q + a] - want) > 1e-14) throw std::runtime_error("unexpected Nt structure");
+        }
+    if (std::fabs(tm.g[q] - 1.0) > 1e-12) throw std::runtime_error("unexpected Ct^{-1} e0");
+    return tm;
+}
+
+// -------------------------------------------------------------------- mesh
+HostMesh make_mesh(int dim, const int n[3], const double *coords) {
+    HostMesh m;
+    m.dim = dim;
+    const int nx = n[0], ny = n[1], nz = dim == 3 ? n[2] : 1;
+    m.n[0] = nx; m.n[1] = ny; m.n[2] = dim == 3 ? nz : 1;
+    auto nid = [&](int i, int j, int k) { return i + (nx + 1) * (j + (ny + 1) * k); };
+    if (dim == 2) {
+        m.n_nodes = (nx + 1) * (ny + 1);
+        m.Ex = nx * (ny + 1); m.Ey = (nx + 1) * ny;
+        m.n_edges = m.Ex + m.Ey;
+        m.n_cells = nx * ny;
+    } else {
+        m.n_nodes = (nx + 1) * (ny + 1) * (nz + 1);
+        m.Ex = nx * (ny + 1) * (nz + 1); m.Ey = (nx + 1) * ny * (nz + 1);
+        m.n_edges = m.Ex + m.Ey + (nx + 1) * (ny + 1) * nz;
+        m.n_cells = nx * ny * nz;
+    }
+    m.coords.resize((size_t)m.n_nodes * dim);
+    if (coords) {
+        std::memcpy(m.coords.data(), coords, sizeof(double) * m.coords.size());
+    } else {
+        const int kmax = dim == 3 ? nz : 0;
+        for (int k = 0; k <= kmax; ++k)
+            for (int j = 0; j <= ny; ++j)
+                for (int i = 0; i <= nx; ++i) {
+                    double *X = &m.coords[(size_t)nid(i, j, k) * dim];
+                    X[0] = (double)i / nx; X[1] = (double)j / ny;
+                    if (dim == 3) X[2] = (double)k / nz;
+                }
+    }
+    m.edge_nodes.resize((size_t)2 * m.n_edges);
+    const int kk = dim == 3 ? nz : 0;
+    // x-edges
+    for (int k = 0; k <= kk; ++k)
+        for (int j = 0; j <= ny; ++j)
+            for (int i = 0; i < nx; ++i) {
+                int e = i + nx * (j + (ny + 1) * k);
+                m.edge_nodes[2 * e] = nid(i, j, k); m.edge_nodes[2 * e + 1] = nid(i + 1, j, k);
+            }
+    for (int k = 0; k <= kk; ++k)
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i <= nx; ++i) {
+                int e = m.Ex + i + (nx + 1) * (j + ny * k);
+                m.edge_nodes[2 * e] = nid(i, j, k); m.edge_nodes[2 * e + 1] = nid(i, j + 1, k);
+            }
+    if (dim == 3)
+        for (int k = 0; k < nz; ++k)
+            for (int j = 0; j <= ny; ++j)
+                for (int i = 0; i <= nx; ++i) {
+                    int e = m.Ex + m.Ey + i + (nx + 1) * (j + (ny + 1) * k);
+                    m.edge_nodes[2 * e] = nid(i, j, k); m.edge_nodes[2 * e + 1] = nid(i, j, k + 1);
+                }
+    const int ne = dim == 3 ? 12 : 4, nn = dim == 3 ? 8 : 4;
+    m.cell_edges.resize((size_t)ne * m.n_cells);
+    m.cell_nodes.resize((size_t)nn * m.n_cells);
+    for (int k = 0; k < (dim == 3 ? nz : 1); ++k)
+        for (int j = 0; j < ny; ++j)
+            for (int i = 0; i < nx; ++i) {
+                const int c = i + nx * (j + ny * k);
+                int *E = &m.cell_edges[(size_t)ne * c];
+                int *N = &m.cell_nodes[(size_t)nn * c];
+                if (dim == 2) {
+                    for (int b = 0; b < 2; ++b) E[b] = i + nx * (j + b);
+                    for (int a = 0; a < 2; ++a) E[2 + a] = m.Ex + (i + a) + (nx + 1) * j;
+                    for (int b = 0; b < 2; ++b)
+                        for (int a = 0; a < 2; ++a) N[a + 2 * b] = nid(i + a, j + b, 0);
+                } else {
+                    for (int c2 = 0; c2 < 2; ++c2)
+                        for (int b = 0; b < 2; ++b) E[b + 2 * c2] = i + nx * ((j + b) + (ny + 1) * (k + c2));
+                    for (int c2 = 0; c2 < 2; ++c2)
+                        for (int a = 0; a < 2; ++a) E[4 + a + 2 * c2] = m.Ex + (i + a) + (nx + 1) * (j + ny * (k + c2));
+                    for (int b = 0; b < 2; ++b)
+                        for (int a = 0; a < 2; ++a)
+                            E[8 + a + 2 * b] = m.Ex + m.Ey + (i + a) + (nx + 1) * ((j + b) + (ny + 1) * k);
+                    for (int c2 = 0; c2 < 2; ++c2)
+                        for (int b = 0; b < 2; ++b)
+                            for (int a = 0; a < 2; ++a) N[a + 2 * b + 4 * c2] = nid(i + a, j + b, k + c2);
+                }
+            }
+    return m;
+}
+
+// ------------------------------------------------------- element integrals
+static inline double l01(int s, double t) { return s ? t : 1.0 - t; }
+static inline double d01(int s) { return s ? 1.0 : -1.0; }
+
+// Reference Nedelec basis (values N[e][3], curls C[e][3]; 2D: C[e][0] = scalar curl)
+static void edge_basis(int dim, const double *p, double N[12][3], double C[12][3]) {
+    std::memset(N, 0, sizeof(double) * 36);
+    std::memset(C, 0, sizeof(double) * 36);
+    if (dim == 2) {
+        const double x = p[0], y = p[1];
+        for (int b = 0; b < 2; ++b) { N[b][0] = l01(b, y); C[b][0] = -d01(b); }
+        for (int a = 0; a < 2; ++a) { N[2 + a][1] = l01(a, x); C[2 + a][0] = d01(a); }
+        return;
+    }
+    const double x = p[0], y = p[1], z = p[2];
+    for (int c = 0; c < 2; ++c)
+        for (int b = 0; b < 2; ++b) {
+            int e = b + 2 * c;
+            N[e][0] = l01(b, y) * l01(c, z);
+            C[e][1] = l01(b, y) * d01(c);
+            C[e][2] = -d01(b) * l01(c, z);
+        }
+    for (int c = 0; c < 2; ++c)
+        for (int a = 0; a < 2; ++a) {
+            int e = 4 + a + 2 * c;
+            N[e][1] = l01(a, x) * l01(c, z);
+            C[e][0] = -l01(a, x) * d01(c);
+            C[e][2] = d01(a) * l01(c, z);
+        }
+    for (int b = 0; b < 2; ++b)
+        for (int a = 0; a < 2; ++a) {
+            int e = 8 + a + 2 * b;
+            N[e][2] = l01(a, x) * l01(b, y);
+            C[e][0] = l01(a, x) * d01(b);
+            C[e][1] = -d01(a) * l01(b, y);
+        }
+}
+
+static void node_grads(int dim, const double *p, double D[8][3]) {
+    const int nl = 1 << dim;
+    for (int n = 0; n < nl; ++n)
+        for (int e = 0; e < dim; ++e) {
+            double v = 1.0;
+            for (int d = 0; d < dim; ++d) {
+                int o = (n >> d) & 1;
+                v *= (d == e) ? d01(o) : l01(o, p[d]);
+            }
+            D[n][e] = v;
+        }
+}
+
+// 2x2 / 3x3 inverse by cofactors (exact zeros stay exact on axis-aligned cells)
+static double inv_small(int d, const double *A, double *B) {
+    if (d == 2) {
+        double det = A[0] * A[3] - A[1] * A[2];
+        B[0] = A[3] / det; B[1] = -A[1] / det; B[2] = -A[2] / det; B[3] = A[0] / det;
+        return det;
+    }
+    double c00 = A[4] * A[8] - A[5] * A[7], c01 = A[5] * A[6] - A[3] * A[8], c02 = A[3] * A[7] - A[4] * A[6];
+    double det = A[0] * c00 + A[1] * c01 + A[2] * c02;
+    B[0] = c00 / det; B[3] = c01 / det; B[6] = c02 / det;
+    B[1] = (A[2] * A[7] - A[1] * A[8]) / det; B[4] = (A[0] * A[8] - A[2] * A[6]) / det; B[7] = (A[1] * A[6] - A[0] * A[7]) / det;
+    B[2] = (A[1] * A[5] - A[2] * A[4]) / det; B[5] = (A[2] * A[3] - A[0] * A[5]) / det; B[8] = (A[0] * A[4] - A[1] * A[3]) / det;
+    return det;
+}
+
+// Element matrices of cell c: Me, Ke (ne x ne), Kne (nn x nn); 3-point Gauss per direction (R5)
+static void element(const HostMesh &m, int c, double sigma, double nu, double *Me, double *Ke, double *Kne) {
+    const int d = m.dim, ne = d == 3 ? 12 : 4, nn = 1 << d;
+    static const double gp[3] = {0.5 - 0.5 * std::sqrt(0.6), 0.5, 0.5 + 0.5 * std::sqrt(0.6)};
+    static const double gw[3] = {5.0 / 18.0, 8.0 / 18.0, 5.0 / 18.0};
+    std::fill(Me, Me + ne * ne, 0.0);
+    std::fill(Ke, Ke + ne * ne, 0.0);
+    std::fill(Kne, Kne + nn * nn, 0.0);
+    const int nq = d == 3 ? 27 : 9;
+    for (int iq = 0; iq < nq; ++iq) {
+        int ix = iq % 3, iy = (iq / 3) % 3, iz = iq / 9;
+        double p[3] = {gp[ix], gp[iy], gp[iz]};
+        double w = gw[ix] * gw[iy] * (d == 3 ? gw[iz] : 1.0);
+        double D[8][3];
+        node_grads(d, p, D);
+        double J[9] = {0};   // J[r*d + col] = dx_r / dxhat_col
+        for (int n = 0; n < nn; ++n) {
+            const double *X = &m.coords[(size_t)m.cell_nodes[(size_t)nn * c + n] * d];
+            for (int r = 0; r < d; ++r)
+                for (int k = 0; k < d; ++k) J[r * d + k] += X[r] * D[n][k];
+        }
+        double JtJ[9] = {0}, G[9];
+        for (int a = 0; a < d; ++a)
+            for (int b = 0; b < d; ++b)
+                for (int r = 0; r < d; ++r) JtJ[a * d + b] += J[r * d + a] * J[r * d + b];
+        double Jinv[9];
+        double det = inv_small(d, J, Jinv);
+        if (!(det > 0)) throw std::runtime_error("inverted or degenerate cell");
+        inv_small(d, JtJ, G);   // (J^T J)^{-1}
+        double N[12][3], C[12][3];
+        edge_basis(d, p, N, C);
+        for (int i = 0; i < ne; ++i)
+            for (int j = 0; j < ne; ++j) {
+                double mv = 0, kv = 0;
+                for (int a = 0; a < d; ++a)
+                    for (int b = 0; b < d; ++b) mv += N[i][a] * G[a * d + b] * N[j][b];
+                if (d == 3) {
+                    for (int a = 0; a < 3; ++a)
+                        for (int b = 0; b < 3; ++b) kv += C[i][a] * JtJ[a * 3 + b] * C[j][b];
+                } else {
+                    kv = C[i][0] * C[j][0];
+                }
+                Me[i * ne + j] += w * sigma * det * mv;
+                Ke[i * ne + j] += w * nu / det * kv;
+            }
+        for (int i = 0; i < nn; ++i)
+            for (int j = 0; j < nn; ++j) {
+                double v = 0;
+                for (int a = 0; a < d; ++a)
+                    for (int b = 0; b < d; ++b) v += D[i][a] * G[a * d + b] * D[j][b];
+                Kne[i * nn + j] += w * sigma * det * v;
+            }
+    }
+}
+
+// ------------------------------------------------------------ ELL assembly
+struct RowAcc {
+    int cap;
+    std::vector<int> col, cnt;
+    std::vector<double> val;
+    RowAcc(int rows, int cap_) : cap(cap_), col((size_t)rows * cap_, -1), cnt(rows, 0), val((size_t)rows * cap_, 0.0) {}
+    void add(int r, int c, double v) {
+        int *C = &col[(size_t)r * cap];
+        for (int s = 0; s < cnt[r]; ++s)
+            if (C[s] == c) { val[(size_t)r * cap + s] += v; return; }
+        if (cnt[r] == cap) throw std::runtime_error("ELL row capacity exceeded");
+        C[cnt[r]] = c; val[(size_t)r * cap + cnt[r]] = v; ++cnt[r];
+    }
+    // compress: sort columns, drop exact zeros, pad with (pad_col(r), 0)
+    HostELL finish(bool square) {
+        HostELL E;
+        E.rows = (int)cnt.size();
+        int width = 0;
+        std::vector<std::vector<std::pair<int, double>>> rows(E.rows);
+        for (int r = 0; r < E.rows; ++r) {
+            for (int s = 0; s < cnt[r]; ++s) {
+                double v = val[(size_t)r * cap + s];
+                if (v != 0.0) rows[r].push_back({col[(size_t)r * cap + s], v});
+            }
+            std::sort(rows[r].begin(), rows[r].end());
+            width = std::max(width, (int)rows[r].size());
+        }
+        E.width = std::max(width, 1);
+        E.col.assign((size_t)E.rows * E.width, 0);
+        E.val.assign((size_t)E.rows * E.width, 0.0);
+        for (int r = 0; r < E.rows; ++r) {
+            for (int s = 0; s < E.width; ++s) {
+                if (s < (int)rows[r].size()) {
+                    E.col[(size_t)r * E.width + s] = rows[r][s].first;
+                    E.val[(size_t)r * E.width + s] = rows[r][s].second;
+                } else {
+                    E.col[(size_t)r * E.width + s] = square ? r : 0;
+                }
+            }
+        }
+        return E;
+    }
+};
+
+static std::vector<double> ell_diag(const HostELL &E) {
+    std::vector<double> d(E.rows, 0.0);
+    for (int r = 0; r < E.rows; ++r)
+        for (int s = 0; s < E.width; ++s)
+            if (E.col[(size_t)r * E.width + s] == r) d[r] += E.val[(size_t)r * E.width + s];
+    return d;
+}
+
+void assemble(HostLevel &L) {
+    const HostMesh &m = L.mesh;
+    const int d = m.dim, ne = d == 3 ? 12 : 4, nn = 1 << d;
+    RowAcc M(m.n_edges, d == 3 ? 40 : 8), K(m.n_edges, d == 3 ? 40 : 8), Kn(m.n_nodes, d == 3 ? 27 : 9);
+    std::vector<double> Me(144), Ke(144), Kne(64);
+    for (int c = 0; c < m.n_cells; ++c) {
+        element(m, c, L.sigma[c], L.nu[c], Me.data(), Ke.data(), Kne.data());
+        const int *E = &m.cell_edges[(size_t)ne * c];
+        const int *N = &m.cell_nodes[(size_t)nn * c];
+        for (int i = 0; i < ne; ++i)
+            for (int j = 0; j < ne; ++j) {
+                M.add(E[i], E[j], Me[i * ne + j]);
+                K.add(E[i], E[j], Ke[i * ne + j]);
+            }
+        for (int i = 0; i < nn; ++i)
+            for (int j = 0; j < nn; ++j) Kn.add(N[i], N[j], Kne[i * nn + j]);
+    }
+    L.M = M.finish(true);
+    L.K = K.finish(true);
+    L.Kn = Kn.finish(true);
+    L.dM = ell_diag(L.M);
+    L.dK = ell_diag(L.K);
+    L.dN = ell_diag(L.Kn);
+    // G^T incidence (node -> +-incident edges)
+    RowAcc gt(m.n_nodes, d == 3 ? 6 : 4);
+    for (int e = 0; e < m.n_edges; ++e) {
+        gt.add(m.edge_nodes[2 * e], 2 * e + 1, 1.0);       // start node: -1
+        gt.add(m.edge_nodes[2 * e + 1], 2 * e, 1.0);       // end node: +1
+    }
+    HostELL GT;
+    GT.rows = m.n_nodes;
+    GT.width = d == 3 ? 6 : 4;
+    GT.col.assign((size_t)GT.rows * GT.width, -1);
+    GT.val.clear();
+    for (int r = 0; r < m.n_nodes; ++r) {
+        std::vector<int> cs(&gt.col[(size_t)r * gt.cap], &gt.col[(size_t)r * gt.cap] + gt.cnt[r]);
+        std::sort(cs.begin(), cs.end());
+        for (size_t s = 0; s < cs.size(); ++s) GT.col[(size_t)r * GT.width + s] = cs[s];
+    }
+    L.GT = GT;
+}
+
+// ------------------------------------------------------------- transfers
+static int edge_id(const HostMesh &m, int dir, const int *ijk) {
+    const int nx = m.n[0], ny = m.n[1];
+    if (m.dim == 2) {
+        if (dir == 0) return ijk[0] + nx * ijk[1];
+        return m.Ex + ijk[0] + (nx + 1) * ijk[1];
+    }
+    if (dir == 0) return ijk[0] + nx * (ijk[1] + (ny + 1) * ijk[2]);
+    if (dir == 1) return m.Ex + ijk[0] + (nx + 1) * (ijk[1] + ny * ijk[2]);
+    return m.Ex + m.Ey + ijk[0] + (nx + 1) * (ijk[1] + (ny + 1) * ijk[2]);
+}
+
+// Canonical Nedelec interpolation of coarse edge functions on the fine edges
+// of a 2:1 refinement (R6): weight 1/2 x (Q1 hat weights across the edge).
+static void build_transfers(const HostMesh &f, const HostMesh &c, HostELL &Pg, HostELL &Rg) {
+    const int d = f.dim;
+    RowAcc P(f.n_edges, d == 3 ? 4 : 2), R(c.n_edges, d == 3 ? 18 : 6);
+    for (int dir = 0; dir < d; ++dir) {
+        int lim[3];
+        for (int a = 0; a < 3; ++a) lim[a] = a < d ? (a == dir ? f.n[a] : f.n[a] + 1) : 1;
+        for (int k = 0; k < lim[2]; ++k)
+            for (int j = 0; j < lim[1]; ++j)
+                for (int i = 0; i < lim[0]; ++i) {
+                    int ijk[3] = {i, j, k};
+                    const int ef = edge_id(f, dir, ijk);
+                    // transverse axes: list of (coarse index, weight)
+                    int cidx[3][2]; double cw[3][2]; int cnt[3];
+                    for (int a = 0; a < d; ++a) {
+                        if (a == dir) { cidx[a][0] = ijk[a] / 2; cw[a][0] = 0.5; cnt[a] = 1; continue; }
+                        if (ijk[a] % 2 == 0) { cidx[a][0] = ijk[a] / 2; cw[a][0] = 1.0; cnt[a] = 1; }
+                        else { cidx[a][0] = (ijk[a] - 1) / 2; cidx[a][1] = (ijk[a] + 1) / 2; cw[a][0] = cw[a][1] = 0.5; cnt[a] = 2; }
+                    }
+                    if (d == 2) { cnt[2] = 1; cidx[2][0] = 0; cw[2][0] = 1.0; }
+                    for (int s0 = 0; s0 < cnt[0]; ++s0)
+                        for (int s1 = 0; s1 < cnt[1]; ++s1)
+                            for (int s2 = 0; s2 < cnt[2]; ++s2) {
+                                int cc[3] = {cidx[0][s0], cidx[1][s1], cidx[2][s2]};
+                                double w = cw[0][s0] * cw[1][s1] * cw[2][s2];
+                                const int ec = edge_id(c, dir, cc);
+                                P.add(ef, ec, w);
+                                R.add(ec, ef, w);
+                            }
+                }
+    }
+    Pg = P.finish(false);
+    Rg = R.finish(false);
+}
+
+static void coarsen_mesh(const HostLevel &F, HostLevel &C) {
+    const HostMesh &f = F.mesh;
+    const int d = f.dim;
+    int nc[3] = {f.n[0] / 2, f.n[1] / 2, d == 3 ? f.n[2] / 2 : 1};
+    std::vector<double> X;
+    const int nxc = nc[0], nyc = nc[1], nzc = d == 3 ? nc[2] : 0;
+    for (int k = 0; k <= nzc; ++k)
+        for (int j = 0; j <= nyc; ++j)
+            for (int i = 0; i <= nxc; ++i) {
+                int fid = 2 * i + (f.n[0] + 1) * (2 * j + (f.n[1] + 1) * 2 * k);
+                for (int a = 0; a < d; ++a) X.push_back(f.coords[(size_t)fid * d + a]);
+            }
+    C.mesh = make_mesh(d, nc, X.data());
+    const int ncc = C.mesh.n_cells, nch = 1 << d;
+    C.sigma.assign(ncc, 0.0); C.nu.assign(ncc, 0.0); C.ratio_min.assign(ncc, 0.0);
+    for (int k = 0; k < (d == 3 ? nc[2] : 1); ++k)
+        for (int j = 0; j < nc[1]; ++j)
+            for (int i = 0; i < nc[0]; ++i) {
+                const int cc = i + nc[0] * (j + nc[1] * k);
+                double s = 0, n = 0, r = 1e300;
+                for (int ch = 0; ch < nch; ++ch) {
+                    int a = ch & 1, b = (ch >> 1) & 1, c2 = (ch >> 2) & 1;
+                    int fc = (2 * i + a) + f.n[0] * ((2 * j + b) + f.n[1] * (2 * k + c2));
+                    s += F.sigma[fc]; n += F.nu[fc]; r = std::min(r, F.ratio_min[fc]);
+                }
+                C.sigma[cc] = s / nch; C.nu[cc] = n / nch; C.ratio_min[cc] = r;
+            }
+}
+
+static double level_lambda(const HostLevel &L) {
+    // Eq. (3): min over cells of min_{x in T}(beta/alpha) * tau / h_T^2, h_T = longest edge (l.109)
+    const HostMesh &m = L.mesh;
+    const int d = m.dim, ne = d == 3 ? 12 : 4;
+    double tmin = *std::min_element(L.tau.begin(), L.tau.end());
+    double lam = 1e300;
+    for (int c = 0; c < m.n_cells; ++c) {
+        double h2 = 0;
+        for (int i = 0; i < ne; ++i) {
+            int e = m.cell_edges[(size_t)ne * c + i];
+            const double *A = &m.coords[(size_t)m.edge_nodes[2 * e] * d];
+            const double *B = &m.coords[(size_t)m.edge_nodes[2 * e + 1] * d];
+            double l2 = 0;
+            for (int a = 0; a < d; ++a) l2 += (B[a] - A[a]) * (B[a] - A[a]);
+            h2 = std::max(h2, l2);
+        }
+        lam = std::min(lam, L.ratio_min[c] * tmin / h2);
+    }
+    return lam;
+}
+
+void build_hierarchy(const st_params &p, const Options &o, const TimeMats &tm, std::vector<HostLevel> &levels) {
+    const int Q = tm.Q, q = Q - 1;
+    levels.clear();
+    levels.emplace_back();
+    {
+        HostLevel &L = levels.back();
+        int n[3] = {p.nx, p.ny, p.nz};
+        L.mesh = make_mesh(p.dim, n, p.coords);
+        L.sigma.assign(p.sigma, p.sigma + L.mesh.n_cells);
+        L.nu.assign(p.nu, p.nu + L.mesh.n_cells);
+        L.ratio_min.resize(L.mesh.n_cells);
+        for (int c = 0; c < L.mesh.n_cells; ++c) L.ratio_min[c] = L.nu[c] / L.sigma[c];
+        L.tau.assign(p.tau, p.tau + p.n_slabs);
+    }
+    for (int lvl = 0;; ++lvl) {
+        HostLevel &L = levels[lvl];
+        assemble(L);
+        const int S = (int)L.tau.size();
+        L.lambda = level_lambda(L);
+        if (S <= o.min_slabs || S % 2) break;
+        const HostMesh &m = L.mesh;
+        bool can = true;
+        for (int a = 0; a < m.dim; ++a) can = can && (m.n[a] % 2 == 0) && m.n[a] >= 2;
+        bool cs = false;
+        if (o.mode == 0) cs = L.lambda >= o.lambda_crit && can;
+        else if (o.mode == 2) cs = lvl == 0 && can;
+        L.space_coarsened = cs;
+        // time transfer matrices per coarse slab (R7): Pt[(j*Q + b)][a] = phi_a(position of fine node (j,b))
+        L.Pt.assign((size_t)(S / 2) * 2 * Q * Q, 0.0);
+        for (int K = 0; K < S / 2; ++K) {
+            const double th = L.tau[2 * K] / (L.tau[2 * K] + L.tau[2 * K + 1]);
+            for (int j = 0; j < 2; ++j)
+                for (int b = 0; b < Q; ++b) {
+                    const double sb = q == 0 ? 0.0 : (double)b / q;
+                    const double pos = j == 0 ? th * sb : th + (1.0 - th) * sb;
+                    for (int a = 0; a < Q; ++a)
+                        L.Pt[(size_t)K * 2 * Q * Q + (j * Q + b) * Q + a] = lag(q, a, pos);
+                }
+        }
+        HostLevel C;
+        if (cs) {
+            coarsen_mesh(L, C);
+            build_transfers(L.mesh, C.mesh, L.Pg, L.Rg);
+        } else {
+            C.mesh = L.mesh; C.sigma = L.sigma; C.nu = L.nu; C.ratio_min = L.ratio_min;
+        }
+        C.tau.resize(S / 2);
+        for (int K = 0; K < S / 2; ++K) C.tau[K] = L.tau[2 * K] + L.tau[2 * K + 1];
+        levels.push_back(std::move(C));
+    }
+    // coarsest level: dense inverse of A_k = Ct (x) M + tau_k Mt (x) K, index a*n + e (R8)
+    HostLevel &Lc = levels.back();
+    const int n = Lc.mesh.n_edges, N = Q * n, S = (int)Lc.tau.size();
+    if ((double)N * N * S > 64.0e6) throw std::length_error("coarsest level too large for the dense solve");
+    Lc.Ainv.assign((size_t)S * N * N, 0.0);
+    std::vector<double> A((size_t)N * N);
+    for (int k = 0; k < S; ++k) {
+        std::fill(A.begin(), A.end(), 0.0);
+        for (int e = 0; e < n; ++e) {
+            for (int s = 0; s < Lc.M.width; ++s) {
+                int c = Lc.M.col[(size_t)e * Lc.M.width + s]; double v = Lc.M.val[(size_t)e * Lc.M.width + s];
+                for (int b = 0; b < Q; ++b)
+                    for (int a = 0; a < Q; ++a) A[(size_t)(b * n + e) * N + a * n + c] += tm.Ct[b * Q + a] * v;
+            }
+            for (int s = 0; s < Lc.K.width; ++s) {
+                int c = Lc.K.col[(size_t)e * Lc.K.width + s]; double v = Lc.K.val[(size_t)e * Lc.K.width + s];
+                for (int b = 0; b < Q; ++b)
+                    for (int a = 0; a < Q; ++a) A[(size_t)(b * n + e) * N + a * n + c] += Lc.tau[k] * tm.Mt[b * Q + a] * v;
+            }
+        }
+        invert(N, A.data(), &Lc.Ainv[(size_t)k * N * N]);
+    }
+}
+
+}  // namespace st

@@ -1,0 +1,152 @@
+"""GPU parity: libst.so (CUDA, through the C-ABI) against the CPU oracle on the
+same seeded inputs (workloads).  Bar (north star): identical V-cycle iteration
+counts, per-iteration relative residuals equal to 1e-10 relative."""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import mesh, multigrid as mg, spacetime as st_oracle
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1911_09548_b200 import build
+    build.build()
+    return torch
+
+
+def oracle_hierarchy(w, **kw):
+    return mg.Hierarchy(mesh.Mesh(w.n, w.node_coords()), w.sigma, w.nu, w.tau, w.q,
+                        mg.Options(omega_s=w.omega_s, **kw))
+
+
+def solver(w, **kw):
+    import paper_1911_09548_b200 as p
+    return p.Solver.from_workload(w, **kw)
+
+
+# (name, maxit) -- stagnating regimes (large lambda with pure Jacobi inner sweeps, sigma=1e-6
+# insulators) are compared over a fixed number of cycles
+CASES = [("c1", 40), ("c2", 40), ("c2_lam0.1", 60), ("c2_lam10", 12), ("c3", 12), ("c4", 40), ("c5", 12)]
+
+
+@pytest.mark.parametrize("name,maxit", CASES)
+def test_solve_parity(torch_cuda, name, maxit):
+    torch = torch_cuda
+    w = workloads.small(name)
+    H = oracle_hierarchy(w)
+    F = workloads.to_oracle(w.rhs())
+    X, hist = mg.solve(H, F, tol=1e-8, maxit=maxit)
+    s = solver(w)
+    f = torch.from_numpy(w.rhs()).cuda()
+    x = torch.zeros_like(f)
+    it, h = s.solve(x, f, tol=1e-8, maxit=maxit)
+    assert it == len(hist) - 1
+    np.testing.assert_allclose(h, hist, rtol=RTOL, atol=0)
+    Xg = workloads.to_oracle(x.cpu().numpy())
+    assert np.linalg.norm(Xg - X) <= 1e-9 * np.linalg.norm(X)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c5"])
+@pytest.mark.parametrize("q", [0, 1, 2])
+def test_vcycle_parity_random_start(torch_cuda, name, q):
+    # one V-cycle from a random x (all smoother branches active), dG degrees 0..2
+    torch = torch_cuda
+    w = workloads.small(name)
+    w.q = q
+    rng = np.random.default_rng(11)
+    F = rng.uniform(-1, 1, (w.S, q + 1, w.n_edges))
+    X0 = rng.uniform(-1, 1, F.shape)
+    H = oracle_hierarchy(w)
+    X1 = mg.vcycle(H, 0, X0.copy(), F)
+    s = solver(w)
+    x = torch.from_numpy(workloads.from_oracle(X0)).cuda()
+    f = torch.from_numpy(workloads.from_oracle(F)).cuda()
+    s.vcycle(x, f)
+    Xg = workloads.to_oracle(x.cpu().numpy())
+    assert np.linalg.norm(Xg - X1) <= 1e-12 * np.linalg.norm(X1)
+
+
+@pytest.mark.parametrize("spec,nu_s,nu_n", [("SAS", 1, 1), ("SAS", 3, 3), ("SA", 2, 2), ("ASSA", 2, 4), ("S", 2, 2)])
+def test_vcycle_parity_smoother_variants(torch_cuda, spec, nu_s, nu_n):
+    torch = torch_cuda
+    w = workloads.small("c5")
+    rng = np.random.default_rng(5)
+    F = rng.uniform(-1, 1, (w.S, w.q + 1, w.n_edges))
+    X0 = rng.uniform(-1, 1, F.shape)
+    H = oracle_hierarchy(w, spec=spec, nu_s=nu_s, nu_n=nu_n)
+    X1 = mg.vcycle(H, 0, X0.copy(), F)
+    s = solver(w, spec=spec, nu_s=nu_s, nu_n=nu_n)
+    x = torch.from_numpy(workloads.from_oracle(X0)).cuda()
+    s.vcycle(x, torch.from_numpy(workloads.from_oracle(F)).cuda())
+    Xg = workloads.to_oracle(x.cpu().numpy())
+    assert np.linalg.norm(Xg - X1) <= 1e-12 * np.linalg.norm(X1)
+
+
+@pytest.mark.parametrize("name", ["c1", "c3", "c5"])
+def test_residual_parity(torch_cuda, name):
+    torch = torch_cuda
+    w = workloads.small(name)
+    rng = np.random.default_rng(3)
+    X = rng.uniform(-1, 1, (w.S, w.q + 1, w.n_edges))
+    F = workloads.to_oracle(w.rhs())
+    H = oracle_hierarchy(w)
+    R = F - st_oracle.apply_L(H.levels[0], X)
+    s = solver(w)
+    x = torch.from_numpy(workloads.from_oracle(X)).cuda()
+    f = torch.from_numpy(w.rhs()).cuda()
+    r = torch.empty_like(f)
+    rn, fn = s.residual(x, f, r, norms=True)
+    Rg = workloads.to_oracle(r.cpu().numpy())
+    np.testing.assert_allclose(Rg, R, rtol=0, atol=1e-13 * np.abs(R).max())
+    assert rn == pytest.approx(np.linalg.norm(R), rel=1e-12)
+    assert fn == pytest.approx(np.linalg.norm(F), rel=1e-12)
+
+
+def test_plan_matches(torch_cuda):
+    w = workloads.small("c3")
+    H = oracle_hierarchy(w)
+    inf = solver(w).info()
+    assert inf["level_n_edges"] == [lv.n for lv in H.levels]
+    assert inf["level_n_slabs"] == [lv.S for lv in H.levels]
+
+
+def test_solve_host_matches_device(torch_cuda):
+    torch = torch_cuda
+    w = workloads.small("c1")
+    s = solver(w)
+    f = w.rhs()
+    xh = np.zeros_like(f)
+    it_h, hist_h = s.solve_host(xh, f, tol=1e-8, maxit=30)
+    x = torch.zeros(f.shape, dtype=torch.float64, device="cuda")
+    it_d, hist_d = s.solve(x, torch.from_numpy(f).cuda(), tol=1e-8, maxit=30)
+    assert it_h == it_d and hist_h == hist_d
+    assert np.array_equal(xh, x.cpu().numpy())
+
+
+def test_zero_rhs_gives_zero(torch_cuda):
+    torch = torch_cuda
+    w = workloads.small("c2")
+    s = solver(w)
+    f = torch.zeros(s.shape, dtype=torch.float64, device="cuda")
+    x = torch.zeros_like(f)
+    s.vcycle(x, f)
+    assert torch.count_nonzero(x).item() == 0
+
+
+def test_deterministic(torch_cuda):
+    torch = torch_cuda
+    w = workloads.small("c5")
+    s = solver(w)
+    f = torch.from_numpy(w.rhs()).cuda()
+    outs = []
+    for _ in range(2):
+        x = torch.zeros_like(f)
+        outs.append((s.solve(x, f, tol=1e-8, maxit=5), x.clone()))
+    assert outs[0][0] == outs[1][0] and torch.equal(outs[0][1], outs[1][1])

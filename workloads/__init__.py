@@ -66,6 +66,16 @@ class Workload:
         f = rng.uniform(-1.0, 1.0, size=(self.S, self.q + 1, self.n_edges))
         return np.ascontiguousarray(f.transpose(2, 1, 0))
 
+    def rhs_device(self, device="cuda"):
+        """Bench-size RHS drawn on the device: the same U(-1,1) i.i.d. recipe and seed, but
+        torch's generator stream (not bit-identical to rhs()); ST layout."""
+        import torch
+        g = torch.Generator(device=device)
+        g.manual_seed(self.rhs_seed)
+        f = torch.empty((self.n_edges, self.q + 1, self.S), dtype=torch.float64, device=device)
+        f.uniform_(-1.0, 1.0, generator=g)
+        return f
+
     def uniform_coords(self):
         axes = [np.linspace(0.0, 1.0, v + 1) for v in self.n]
         grids = np.meshgrid(*axes[::-1], indexing="ij")[::-1]
