@@ -215,6 +215,9 @@ def run_ours(args, rank, world, local_rank):
                    "d2h_bytes_per_step": f.numel() * 8,
                    "note": "st_solve_host(maxit=1): H2D f,x from pinned memory, ||f||, ||r||, one V-cycle, "
                            "||r||, D2H x"}
+    info = s.info()
+    s.close()
+    torch.cuda.synchronize()
     if rank != 0:
         return
     peak, peak_src = measured_peak()
@@ -228,7 +231,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args), "rhs": "U(-1,1) drawn on the device (torch generator, seed 3)", "n_edges": s.n_edges, "slabs_per_gpu": args.slabs,
-                   "dofs_per_gpu": n_dofs, "levels": s.info()["n_levels"],
+                   "dofs_per_gpu": n_dofs, "levels": info["n_levels"],
                    "l2": f"no flush: every space-time vector is {8 * n_dofs / 1e9:.2f} GB >> 126 MB L2",
                    "parallelism": f"slab blocks, {world} replica(s)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -175,6 +175,9 @@ class Solver:
             self._h = None
 
     def __del__(self):
+        import sys
+        if sys.is_finalizing():
+            return          # the CUDA context may already be gone; the process exit frees everything
         try:
             self.close()
         except Exception:

@@ -99,8 +99,13 @@ struct st_handle {
     st::DevELL upload(const st::HostELL &E) {
         st::DevELL d;
         d.rows = E.rows; d.width = E.width;
-        d.col = upload(E.col);
-        if (!E.val.empty()) d.val = upload(E.val);
+        if (E.val.empty()) {
+            d.col = upload(E.col);
+        } else {
+            std::vector<st::Ent> ent(E.col.size());
+            for (size_t i = 0; i < ent.size(); ++i) ent[i] = st::Ent{E.val[i], E.col[i], 0};
+            d.e = upload(ent);
+        }
         return d;
     }
     ~st_handle() {
@@ -119,7 +124,7 @@ size_t vec_len(const DevLevel &L, int Q, bool nodes = false) {
 }
 
 // Algorithmic bytes: every vector touched once, operators read once.
-double ell_bytes(const st::DevELL &E) { return (double)E.rows * E.width * 12.0; }
+double ell_bytes(const st::DevELL &E) { return (double)E.rows * E.width * 16.0; }
 double op_bytes(const DevLevel &L) { return ell_bytes(L.M) + ell_bytes(L.K) + 16.0 * L.n_edges; }
 double evec(const DevLevel &L, int Q) { return 8.0 * L.n_edges * Q * L.S; }
 double nvec(const DevLevel &L, int Q) { return 8.0 * L.n_nodes * Q * L.S; }
@@ -297,6 +302,9 @@ int st_setup(const st_params *p, st_handle **out) {
             D.M = h->upload(H.M); D.K = h->upload(H.K); D.Kn = h->upload(H.Kn); D.GT = h->upload(H.GT);
             D.dM = h->upload(H.dM); D.dK = h->upload(H.dK); D.dN = h->upload(H.dN);
             D.edge_nodes = h->upload(H.mesh.edge_nodes);
+            D.sched_e = h->upload(H.sched_e); D.bptr_e = h->upload(H.bptr_e);
+            D.sched_n = h->upload(H.sched_n); D.bptr_n = h->upload(H.bptr_n);
+            D.nbox_e = (int)H.bptr_e.size() - 1; D.nbox_n = (int)H.bptr_n.size() - 1;
             D.tau = h->upload(H.tau);
             D.space_coarsened = H.space_coarsened;
             const bool coarsest = l + 1 == h->hl.size();
@@ -318,6 +326,7 @@ int st_setup(const st_params *p, st_handle **out) {
                 if (o.nu_n > 2) { D.wn = h->dalloc<double>(vn); D.zn2 = h->dalloc<double>(vn); }
             }
             max_partial = std::max(max_partial, (ve + 255) / 256);
+            max_partial = std::max(max_partial, (size_t)st::residual_partials(D));
             // the device owns the operators now; keep only the metadata on the host
             H.M = H.K = H.Kn = H.GT = H.Pg = H.Rg = st::HostELL();
             std::vector<double>().swap(H.Ainv);
@@ -325,6 +334,7 @@ int st_setup(const st_params *p, st_handle **out) {
             std::vector<int>().swap(H.mesh.cell_edges);
             std::vector<int>().swap(H.mesh.cell_nodes);
             std::vector<int>().swap(H.mesh.edge_nodes);
+            std::vector<int>().swap(H.sched_e); std::vector<int>().swap(H.sched_n);
         }
         h->partial = h->dalloc<double>(max_partial);
         h->partial_cap = (int)max_partial;

@@ -26,10 +26,17 @@ struct HostELL {
     std::vector<double> val;
 };
 
+// packed ELL entry: one 16-byte (warp-broadcast) load per nonzero
+struct __attribute__((aligned(16))) Ent {
+    double v;
+    int c;
+    int pad;
+};
+
 struct DevELL {
     int rows = 0, width = 0;
-    int *col = nullptr;
-    double *val = nullptr;
+    Ent *e = nullptr;       // [row][slot]
+    int *col = nullptr;     // only for index-only operators (G^T incidence)
 };
 
 struct HostMesh {
@@ -55,6 +62,8 @@ struct HostLevel {
     HostELL Rg;                                 // coarse edge -> fine edges (restriction rows)
     std::vector<double> Pt;                     // per coarse slab: (2Q x Q) time prolongation, row-major
     std::vector<double> Ainv;                   // coarsest only: per slab dense (QN x QN)
+    // box schedules: rows ordered by small node boxes (box b = rows sched[bptr[b] .. bptr[b+1]))
+    std::vector<int> sched_e, bptr_e, sched_n, bptr_n;
 };
 
 struct DevLevel {
@@ -62,6 +71,8 @@ struct DevLevel {
     DevELL M, K, Kn, GT, Pg, Rg;
     double *dM = nullptr, *dK = nullptr, *dN = nullptr;
     int *edge_nodes = nullptr;
+    int *sched_e = nullptr, *bptr_e = nullptr, *sched_n = nullptr, *bptr_n = nullptr;
+    int nbox_e = 0, nbox_n = 0;
     double *tau = nullptr;
     double *Pt = nullptr;
     double *Ainv = nullptr;
@@ -108,6 +119,7 @@ void launch_prolong(Stream st, const DevLevel &F, int Q, const double *xc, doubl
 int launch_coarsest(Stream st, const DevLevel &L, int Q, const double *f, double *x);
 void launch_reduce(Stream st, int n, const double *partial, double *out);
 int launch_norm2(Stream st, size_t n, const double *v, double *partial);
+int residual_partials(const DevLevel &L);
 
 // setup.cpp
 TimeMats time_matrices(int q);

@@ -82,81 +82,219 @@ __device__ __forceinline__ double block_reduce_sum(double v, double *sh) {
     return v;
 }
 
-// (M x)_a and (K x)_a of row `row`, slab k, plus the M-image of the previous
-// slab's end value (time node q of slab k-1, or prev[col] for k = 0).
-template <int Q, bool COUPLE>
-__device__ __forceinline__ void spatial_apply(const DevELL &M, const DevELL &K, int row, int k, int S,
-                                              const double *__restrict__ x, const double *__restrict__ prev,
-                                              double *mx, double *kx, double &mp) {
-    const int QS = Q * S;
+// Thread mapping of the row kernels: LPR lanes cover one row,
+// each lane SPL (= 2 when S is even) consecutive slabs via 16-byte loads; a warp
+// covers 32/LPR rows, a CTA 8 warps.  Blocks are ordered slab-chunk-major so
+// the CTAs resident at any moment work on the same chunk of LPR*SPL slabs of
+// neighbouring rows: the x rows they gather stay in L2 (working set ~ 3 planes
+// of rows x one chunk instead of 3 planes x all slabs).
+struct Map {
+    int rows, S, spl, lpr_log2, rpw, rows_per_cta, n_rowblocks, chunk, n_chunks;
+};
+
+__device__ __forceinline__ bool map_thread(const Map &m, int &row, int &k0) {
+    const int chunk = blockIdx.x / m.n_rowblocks;
+    const int rb = blockIdx.x - chunk * m.n_rowblocks;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    row = rb * m.rows_per_cta + warp * m.rpw + (lane >> m.lpr_log2);
+    k0 = chunk * m.chunk + (lane & ((1 << m.lpr_log2) - 1)) * m.spl;
+    return row < m.rows && k0 < m.S;
+}
+
+// Box-scheduled mapping: CTA = (slab chunk, node box); its warps
+// loop over the box's rows (sched[bptr[b] .. bptr[b+1])), LPR lanes per row,
+// SPL slabs per lane.  Rows of one box share most of their ELL columns, so a
+// column's x chunk is fetched from L2 once per CTA and re-read from L1.
+struct BoxMap {
+    int S, spl, lpr_log2, rpw, chunk, n_boxes;
+    const int *sched, *bptr;
+};
+
+// Warp-uniform loop: every lane runs the same number of iterations (so row-group
+// shuffles are safe); lanes without work get valid = false, a clamped in-bounds
+// row/slab, and must not store.
+template <class F>
+__device__ __forceinline__ void box_loop(const BoxMap &m, F &&body) {
+    const int chunk = blockIdx.x / m.n_boxes;
+    const int b = blockIdx.x - chunk * m.n_boxes;
+    const int beg = __ldg(m.bptr + b), end = __ldg(m.bptr + b + 1);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k0 = chunk * m.chunk + (lane & ((1 << m.lpr_log2) - 1)) * m.spl;
+    const bool kval = k0 < m.S;
+    const int step = (blockDim.x >> 5) * m.rpw;
+    for (int ib = beg + warp * m.rpw; ib < end; ib += step) {
+        const int i = ib + (lane >> m.lpr_log2);
+        const bool valid = kval && i < end;
+        body(__ldg(m.sched + (i < end ? i : beg)), kval ? k0 : 0, valid);
+    }
+}
+
+__device__ __forceinline__ void ld_ent(const Ent *p, double &v, int &c) {
+    const double2 t = __ldg(reinterpret_cast<const double2 *>(p));
+    v = t.x;
+    c = (int)(unsigned long long)__double_as_longlong(t.y);
+}
+
+template <int SPL>
+__device__ __forceinline__ void ldv(const double *__restrict__ p, double *v) {
+    if constexpr (SPL == 2) {
+        const double2 t = __ldg(reinterpret_cast<const double2 *>(p));
+        v[0] = t.x; v[1] = t.y;
+    } else {
+        v[0] = __ldg(p);
+    }
+}
+
+template <int SPL>
+__device__ __forceinline__ void ldv_rw(const double *p, double *v) {   // data this kernel also writes
+    if constexpr (SPL == 2) {
+        const double2 t = *reinterpret_cast<const double2 *>(p);
+        v[0] = t.x; v[1] = t.y;
+    } else {
+        v[0] = *p;
+    }
+}
+
+template <int SPL>
+__device__ __forceinline__ void stv(double *p, const double *v) {
+    if constexpr (SPL == 2) *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
+    else p[0] = v[0];
+}
+
+// (M x)[a][j], (K x)[a][j] of row `row` at slabs k0+j.  WM/WK > 0: compile-time
+// ELL widths (full unroll: all gathers of a row in flight); 0: runtime width.
+template <int Q, int SPL, int WM, int WK>
+__device__ __forceinline__ void spatial_apply(const DevELL &M, const DevELL &K, int row, int k0, int S,
+                                              const double *__restrict__ x,
+                                              double (&mx)[Q][SPL], double (&kx)[Q][SPL]) {
+    const size_t QS = (size_t)Q * S;
 #pragma unroll
-    for (int a = 0; a < Q; ++a) { mx[a] = 0.0; kx[a] = 0.0; }
-    mp = 0.0;
-    const int *cM = M.col + (size_t)row * M.width;
-    const double *vM = M.val + (size_t)row * M.width;
-#pragma unroll 4
-    for (int s = 0; s < M.width; ++s) {
-        const int c = __ldg(cM + s);
-        const double v = __ldg(vM + s);
-        const double *xc = x + (size_t)c * QS + k;
+    for (int a = 0; a < Q; ++a)
 #pragma unroll
-        for (int a = 0; a < Q; ++a) mx[a] = fma(v, __ldg(xc + a * S), mx[a]);
-        if (COUPLE) {
-            const double xp = k > 0 ? __ldg(xc + (Q - 1) * S - 1) : (prev ? __ldg(prev + c) : 0.0);
-            mp = fma(v, xp, mp);
+        for (int j = 0; j < SPL; ++j) { mx[a][j] = 0.0; kx[a][j] = 0.0; }
+    const Ent *eM = M.e + (size_t)row * (WM > 0 ? WM : M.width);
+    const int wm = WM > 0 ? WM : M.width;
+#pragma unroll (WM > 0 ? WM : 3)
+    for (int s = 0; s < wm; ++s) {
+        double v; int c;
+        ld_ent(eM + s, v, c);
+        const double *xc = x + (size_t)c * QS + k0;
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+            double xv[SPL];
+            ldv<SPL>(xc + a * S, xv);
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) mx[a][j] = fma(v, xv[j], mx[a][j]);
         }
     }
-    const int *cK = K.col + (size_t)row * K.width;
-    const double *vK = K.val + (size_t)row * K.width;
-#pragma unroll 4
-    for (int s = 0; s < K.width; ++s) {
-        const int c = __ldg(cK + s);
-        const double v = __ldg(vK + s);
-        const double *xc = x + (size_t)c * QS + k;
+    const Ent *eK = K.e + (size_t)row * (WK > 0 ? WK : K.width);
+    const int wk = WK > 0 ? WK : K.width;
+#pragma unroll (WK > 0 ? 11 : 3)
+    for (int s = 0; s < wk; ++s) {
+        double v; int c;
+        ld_ent(eK + s, v, c);
+        const double *xc = x + (size_t)c * QS + k0;
 #pragma unroll
-        for (int a = 0; a < Q; ++a) kx[a] = fma(v, __ldg(xc + a * S), kx[a]);
+        for (int a = 0; a < Q; ++a) {
+            double xv[SPL];
+            ldv<SPL>(xc + a * S, xv);
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) kx[a][j] = fma(v, xv[j], kx[a][j]);
+        }
+    }
+}
+
+// Upwind coupling (Nt (x) M) x_{k-1} = e_0 (M x)[q][k-1]: the previous slab's M-image
+// is the own lane's (j >= 1) or the previous lane's (j = 0) already computed mx[q];
+// only the first lane of a row group (k0 at a chunk start) gathers it explicitly.
+template <int Q, int SPL, int WM>
+__device__ __forceinline__ void coupling(const DevELL &M, int row, int k0, int S, int lpr,
+                                         const double *__restrict__ x, const double *__restrict__ prev,
+                                         const double (&mx)[Q][SPL], double (&mp)[SPL]) {
+#pragma unroll
+    for (int j = 1; j < SPL; ++j) mp[j] = mx[Q - 1][j - 1];
+    const double up = __shfl_up_sync(0xffffffffu, mx[Q - 1][SPL - 1], 1, lpr);
+    const int lane_in_row = (threadIdx.x & 31) & (lpr - 1);
+    if (lane_in_row != 0) {
+        mp[0] = up;
+    } else {
+        double acc = 0.0;
+        const int wm = WM > 0 ? WM : M.width;
+        const Ent *eM = M.e + (size_t)row * wm;
+        if (k0 > 0) {
+            for (int s = 0; s < wm; ++s) {
+                double v; int c;
+                ld_ent(eM + s, v, c);
+                acc = fma(v, __ldg(x + (size_t)c * Q * S + (Q - 1) * S + k0 - 1), acc);
+            }
+        } else if (prev) {
+            for (int s = 0; s < wm; ++s) {
+                double v; int c;
+                ld_ent(eM + s, v, c);
+                acc = fma(v, __ldg(prev + c), acc);
+            }
+        }
+        mp[0] = acc;
     }
 }
 
 // ------------------------------------------------------------ residual
 // r = f - L x; optionally z = omega_s D^{-1} r (first Jacobi sweep of B from zero)
 // and per-block partial sums of |r|^2.
-template <int Q, bool R_OUT, bool Z_OUT, bool NORM>
-__global__ void __launch_bounds__(kBlock) k_residual(int rows, int S, DevELL M, DevELL K,
-                                                     const double *__restrict__ tau, const double *__restrict__ x,
-                                                     const double *__restrict__ f, const double *__restrict__ prev,
-                                                     double *__restrict__ r, double *__restrict__ z,
-                                                     const double *__restrict__ dM, const double *__restrict__ dK,
-                                                     double omega_s, KT kt, double *__restrict__ partial) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+template <int Q, int SPL, int WM, int WK, bool R_OUT, bool Z_OUT, bool NORM>
+__global__ void __launch_bounds__(kBlock) k_residual(BoxMap m, DevELL M, DevELL K, const double *__restrict__ tau,
+                                                     const double *__restrict__ x, const double *__restrict__ f,
+                                                     const double *__restrict__ prev, double *__restrict__ r,
+                                                     double *__restrict__ z, const double *__restrict__ dM,
+                                                     const double *__restrict__ dK, double omega_s, KT kt,
+                                                     double *__restrict__ partial) {
     double nrm = 0.0;
-    if (idx < rows * S) {
-        const int row = idx / S, k = idx - row * S;
-        double mx[Q], kx[Q], mp;
-        spatial_apply<Q, true>(M, K, row, k, S, x, prev, mx, kx, mp);
-        const double t = __ldg(tau + k);
-        const size_t base = (size_t)row * Q * S + k;
-        double rr[Q];
+    box_loop(m, [&](int row, int k0, bool valid) {
+        const int S = m.S;
+        double mx[Q][SPL], kx[Q][SPL], mp[SPL];
+        spatial_apply<Q, SPL, WM, WK>(M, K, row, k0, S, x, mx, kx);
+        coupling<Q, SPL, WM>(M, row, k0, S, 1 << m.lpr_log2, x, prev, mx, mp);
+        if (!valid) return;
+        double t[SPL];
+        ldv<SPL>(tau + k0, t);
+        const size_t base = (size_t)row * Q * S + k0;
+        double rr[Q][SPL];
 #pragma unroll
         for (int b = 0; b < Q; ++b) {
-            double acc = 0.0;
+            double fv[SPL];
+            ldv<SPL>(f + base + b * S, fv);
 #pragma unroll
-            for (int a = 0; a < Q; ++a) acc += kt.Ct[b * Q + a] * mx[a] + t * kt.Mt[b * Q + a] * kx[a];
-            rr[b] = __ldg(f + base + b * S) - acc + (b == 0 ? mp : 0.0);
+            for (int j = 0; j < SPL; ++j) {
+                double acc = 0.0;
+#pragma unroll
+                for (int a = 0; a < Q; ++a) acc += kt.Ct[b * Q + a] * mx[a][j] + t[j] * kt.Mt[b * Q + a] * kx[a][j];
+                rr[b][j] = fv[j] - acc + (b == 0 ? mp[j] : 0.0);
+            }
         }
         if (R_OUT)
 #pragma unroll
-            for (int b = 0; b < Q; ++b) r[base + b * S] = rr[b];
+            for (int b = 0; b < Q; ++b) stv<SPL>(r + base + b * S, rr[b]);
         if (Z_OUT) {
-            double y[Q];
-            block_solve<Q>(kt, __ldg(dM + row), __ldg(dK + row), t, rr, y);
+            const double dm = __ldg(dM + row), dk = __ldg(dK + row);
+            double zz[Q][SPL];
 #pragma unroll
-            for (int b = 0; b < Q; ++b) z[base + b * S] = omega_s * y[b];
+            for (int j = 0; j < SPL; ++j) {
+                double v[Q], y[Q];
+#pragma unroll
+                for (int b = 0; b < Q; ++b) v[b] = rr[b][j];
+                block_solve<Q>(kt, dm, dk, t[j], v, y);
+#pragma unroll
+                for (int b = 0; b < Q; ++b) zz[b][j] = omega_s * y[b];
+            }
+#pragma unroll
+            for (int b = 0; b < Q; ++b) stv<SPL>(z + base + b * S, zz[b]);
         }
         if (NORM)
 #pragma unroll
-            for (int b = 0; b < Q; ++b) nrm += rr[b] * rr[b];
-    }
+            for (int b = 0; b < Q; ++b)
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) nrm += rr[b][j] * rr[b][j];
+    });
     if (NORM) {
         __shared__ double sh[kBlock / 32];
         const double s = block_reduce_sum(nrm, sh);
@@ -169,44 +307,64 @@ __global__ void __launch_bounds__(kBlock) k_residual(int rows, int S, DevELL M, 
 // right after the fused first one, reconstructed pointwise as r = D z / omega_s.
 // LAST: x += omega * znew (the smoother update of Eq. 2), in place (x is only
 // read at its own row).
-template <int Q, bool LAST, bool RECON>
-__global__ void __launch_bounds__(kBlock) k_sweep(int rows, int S, DevELL M, DevELL K, const double *__restrict__ tau,
+template <int Q, int SPL, int WM, int WK, bool LAST, bool RECON>
+__global__ void __launch_bounds__(kBlock) k_sweep(BoxMap m, DevELL M, DevELL K, const double *__restrict__ tau,
                                                   const double *__restrict__ dM, const double *__restrict__ dK,
                                                   const double *__restrict__ z, const double *__restrict__ r,
-                                                  double *__restrict__ out, double omega_s, double omega, KT kt) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= rows * S) return;
-    const int row = idx / S, k = idx - row * S;
-    double mz[Q], kz[Q], dummy;
-    spatial_apply<Q, false>(M, K, row, k, S, z, nullptr, mz, kz, dummy);
-    const double t = __ldg(tau + k), dm = __ldg(dM + row), dk = __ldg(dK + row);
-    const size_t base = (size_t)row * Q * S + k;
-    double zr[Q], rr[Q], d[Q], y[Q];
+                                                  double *out, double omega_s, double omega, KT kt) {
+    box_loop(m, [&](int row, int k0, bool valid) {
+    const int S = m.S;
+    double mz[Q][SPL], kz[Q][SPL];
+    spatial_apply<Q, SPL, WM, WK>(M, K, row, k0, S, z, mz, kz);
+    if (!valid) return;
+    double t[SPL];
+    ldv<SPL>(tau + k0, t);
+    const double dm = __ldg(dM + row), dk = __ldg(dK + row);
+    const size_t base = (size_t)row * Q * S + k0;
+    double zr[Q][SPL], rr[Q][SPL], res[Q][SPL];
 #pragma unroll
-    for (int a = 0; a < Q; ++a) zr[a] = z[base + a * S];
-    if (RECON) {
-        block_mul<Q>(kt, dm, dk, t, zr, rr);
+    for (int a = 0; a < Q; ++a) ldv<SPL>(z + base + a * S, zr[a]);
+    if (!RECON)
 #pragma unroll
-        for (int a = 0; a < Q; ++a) rr[a] /= omega_s;
-    } else {
+        for (int a = 0; a < Q; ++a) ldv<SPL>(r + base + a * S, rr[a]);
 #pragma unroll
-        for (int a = 0; a < Q; ++a) rr[a] = __ldg(r + base + a * S);
+    for (int j = 0; j < SPL; ++j) {
+        double v[Q], rv[Q], d[Q], y[Q];
+#pragma unroll
+        for (int a = 0; a < Q; ++a) v[a] = zr[a][j];
+        if (RECON) {
+            block_mul<Q>(kt, dm, dk, t[j], v, rv);
+#pragma unroll
+            for (int a = 0; a < Q; ++a) rv[a] /= omega_s;
+        } else {
+#pragma unroll
+            for (int a = 0; a < Q; ++a) rv[a] = rr[a][j];
+        }
+#pragma unroll
+        for (int b = 0; b < Q; ++b) {
+            double acc = 0.0;
+#pragma unroll
+            for (int a = 0; a < Q; ++a) acc += kt.Ct[b * Q + a] * mz[a][j] + t[j] * kt.Mt[b * Q + a] * kz[a][j];
+            d[b] = rv[b] - acc;
+        }
+        block_solve<Q>(kt, dm, dk, t[j], d, y);
+#pragma unroll
+        for (int a = 0; a < Q; ++a) res[a][j] = zr[a][j] + omega_s * y[a];
     }
-#pragma unroll
-    for (int b = 0; b < Q; ++b) {
-        double acc = 0.0;
-#pragma unroll
-        for (int a = 0; a < Q; ++a) acc += kt.Ct[b * Q + a] * mz[a] + t * kt.Mt[b * Q + a] * kz[a];
-        d[b] = rr[b] - acc;
-    }
-    block_solve<Q>(kt, dm, dk, t, d, y);
     if (LAST) {
 #pragma unroll
-        for (int a = 0; a < Q; ++a) out[base + a * S] += omega * (zr[a] + omega_s * y[a]);
+        for (int a = 0; a < Q; ++a) {
+            double xv[SPL];
+            ldv_rw<SPL>(out + base + a * S, xv);
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) xv[j] += omega * res[a][j];
+            stv<SPL>(out + base + a * S, xv);
+        }
     } else {
 #pragma unroll
-        for (int a = 0; a < Q; ++a) out[base + a * S] = zr[a] + omega_s * y[a];
+        for (int a = 0; a < Q; ++a) stv<SPL>(out + base + a * S, res[a]);
     }
+});
 }
 
 template <int Q>
@@ -217,66 +375,92 @@ __global__ void __launch_bounds__(kBlock) k_axpy(size_t n, double alpha, const d
 
 // ------------------------------------------------------- nodal correction
 // w = G^T r at (node, k); zn = omega_n w / dN (first Jacobi sweep on K_n)
-template <int Q, bool W_OUT>
-__global__ void __launch_bounds__(kBlock) k_gt(int nodes, int S, DevELL GT, const double *__restrict__ r,
+template <int Q, int SPL, bool W_OUT>
+__global__ void __launch_bounds__(kBlock) k_gt(BoxMap m, DevELL GT, const double *__restrict__ r,
                                                const double *__restrict__ dN, double omega_n,
                                                double *__restrict__ zn, double *__restrict__ w) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= nodes * S) return;
-    const int node = idx / S, k = idx - node * S;
-    double acc[Q];
+    box_loop(m, [&](int node, int k0, bool valid) {
+    if (!valid) return;
+    const int S = m.S;
+    double acc[Q][SPL];
 #pragma unroll
-    for (int a = 0; a < Q; ++a) acc[a] = 0.0;
+    for (int a = 0; a < Q; ++a)
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) acc[a][j] = 0.0;
     const int *c = GT.col + (size_t)node * GT.width;
     for (int s = 0; s < GT.width; ++s) {
         const int code = __ldg(c + s);
         if (code < 0) break;
         const double sg = (code & 1) ? -1.0 : 1.0;
-        const double *re = r + (size_t)(code >> 1) * Q * S + k;
+        const double *re = r + (size_t)(code >> 1) * Q * S + k0;
 #pragma unroll
-        for (int a = 0; a < Q; ++a) acc[a] = fma(sg, __ldg(re + a * S), acc[a]);
+        for (int a = 0; a < Q; ++a) {
+            double v[SPL];
+            ldv<SPL>(re + a * S, v);
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) acc[a][j] = fma(sg, v[j], acc[a][j]);
+        }
     }
     const double inv = omega_n / __ldg(dN + node);
-    const size_t base = (size_t)node * Q * S + k;
+    const size_t base = (size_t)node * Q * S + k0;
 #pragma unroll
     for (int a = 0; a < Q; ++a) {
-        zn[base + a * S] = acc[a] * inv;
-        if (W_OUT) w[base + a * S] = acc[a];
+        double zv[SPL];
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) zv[j] = acc[a][j] * inv;
+        stv<SPL>(zn + base + a * S, zv);
+        if (W_OUT) stv<SPL>(w + base + a * S, acc[a]);
     }
+});
 }
 
 // middle nodal sweep: zout = z + omega_n (w - K_n z)/dN
-template <int Q>
-__global__ void __launch_bounds__(kBlock) k_node_sweep(int nodes, int S, DevELL Kn, const double *__restrict__ dN,
+template <int Q, int SPL>
+__global__ void __launch_bounds__(kBlock) k_node_sweep(BoxMap m, DevELL Kn, const double *__restrict__ dN,
                                                        const double *__restrict__ z, const double *__restrict__ w,
                                                        double omega_n, double *__restrict__ zout) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= nodes * S) return;
-    const int node = idx / S, k = idx - node * S;
-    double kz[Q];
+    box_loop(m, [&](int node, int k0, bool valid) {
+    if (!valid) return;
+    const int S = m.S;
+    double kz[Q][SPL];
 #pragma unroll
-    for (int a = 0; a < Q; ++a) kz[a] = 0.0;
-    const int *cc = Kn.col + (size_t)node * Kn.width;
-    const double *vv = Kn.val + (size_t)node * Kn.width;
+    for (int a = 0; a < Q; ++a)
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) kz[a][j] = 0.0;
+    const Ent *en = Kn.e + (size_t)node * Kn.width;
     for (int s = 0; s < Kn.width; ++s) {
-        const double *zc = z + (size_t)__ldg(cc + s) * Q * S + k;
-        const double v = __ldg(vv + s);
+        double v; int c;
+        ld_ent(en + s, v, c);
+        const double *zc = z + (size_t)c * Q * S + k0;
 #pragma unroll
-        for (int a = 0; a < Q; ++a) kz[a] = fma(v, __ldg(zc + a * S), kz[a]);
+        for (int a = 0; a < Q; ++a) {
+            double zv[SPL];
+            ldv<SPL>(zc + a * S, zv);
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) kz[a][j] = fma(v, zv[j], kz[a][j]);
+        }
     }
     const double d = __ldg(dN + node);
-    const size_t base = (size_t)node * Q * S + k;
+    const size_t base = (size_t)node * Q * S + k0;
 #pragma unroll
-    for (int a = 0; a < Q; ++a) zout[base + a * S] = z[base + a * S] + omega_n * (w[base + a * S] - kz[a]) / d;
+    for (int a = 0; a < Q; ++a) {
+        double zv[SPL], wv[SPL];
+        ldv<SPL>(z + base + a * S, zv);
+        ldv<SPL>(w + base + a * S, wv);
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) zv[j] = zv[j] + omega_n * (wv[j] - kz[a][j]) / d;
+        stv<SPL>(zout + base + a * S, zv);
+    }
+});
 }
 
 // Last nodal step fused with the time integration Sigma_t (R2): one warp per
-// node row walks the slabs in chunks of 32; per slab
+// node row walks the slabs in chunks of 32*SPL; per slab
 //   z2 = z + omega_n (w - K_n z)/dN          (MODE 1: w = dN z/omega_n; MODE 2: w read; MODE 0: z2 = z)
-//   s_k = (Ct^{-1} z2)_q,  e_k = carry + sum_{j<=k} s_j   (warp inclusive scan)
+//   s_k = (Ct^{-1} z2)_q,  e_k = carry + sum_{j<=k} s_j   (lane-local pair + warp inclusive scan)
 //   y_k = Ct^{-1} z2 + g e_{k-1},  g = Ct^{-1} e_0
 // tot (optional) receives the row's e_{S-1} (rank carry for multi-GPU slabs).
-template <int Q, int MODE>
+template <int Q, int SPL, int MODE>
 __global__ void __launch_bounds__(kBlock) k_node_scan(int nodes, int S, DevELL Kn, const double *__restrict__ dN,
                                                       const double *__restrict__ z, const double *__restrict__ w,
                                                       double omega_n, KT kt, const double *__restrict__ carry_in,
@@ -288,97 +472,139 @@ __global__ void __launch_bounds__(kBlock) k_node_scan(int nodes, int S, DevELL K
     const double d = __ldg(dN + node);
     const size_t base = (size_t)node * Q * S;
     double carry = carry_in ? __ldg(carry_in + node) : 0.0;
-    const int *cc = Kn.col + (size_t)node * Kn.width;
-    const double *vv = Kn.val + (size_t)node * Kn.width;
-    for (int k0 = 0; k0 < S; k0 += 32) {
-        const int k = k0 + lane;
-        const bool valid = k < S;
-        double z2[Q];
+    const Ent *en = Kn.e + (size_t)node * Kn.width;
+    for (int kc = 0; kc < S; kc += 32 * SPL) {
+        const int k0 = kc + lane * SPL;
+        const bool valid = k0 < S;
+        double z2[Q][SPL];
 #pragma unroll
-        for (int a = 0; a < Q; ++a) z2[a] = 0.0;
+        for (int a = 0; a < Q; ++a)
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) z2[a][j] = 0.0;
         if (valid) {
-            double zr[Q];
+            double zr[Q][SPL];
 #pragma unroll
-            for (int a = 0; a < Q; ++a) zr[a] = z[base + a * S + k];
+            for (int a = 0; a < Q; ++a) ldv<SPL>(z + base + a * S + k0, zr[a]);
             if (MODE == 0) {
 #pragma unroll
-                for (int a = 0; a < Q; ++a) z2[a] = zr[a];
+                for (int a = 0; a < Q; ++a)
+#pragma unroll
+                    for (int j = 0; j < SPL; ++j) z2[a][j] = zr[a][j];
             } else {
-                double kz[Q];
+                double kz[Q][SPL];
 #pragma unroll
-                for (int a = 0; a < Q; ++a) kz[a] = 0.0;
+                for (int a = 0; a < Q; ++a)
+#pragma unroll
+                    for (int j = 0; j < SPL; ++j) kz[a][j] = 0.0;
                 for (int s = 0; s < Kn.width; ++s) {
-                    const double *zc = z + (size_t)__ldg(cc + s) * Q * S + k;
-                    const double v = __ldg(vv + s);
+                    double v; int c;
+                    ld_ent(en + s, v, c);
+                    const double *zc = z + (size_t)c * Q * S + k0;
 #pragma unroll
-                    for (int a = 0; a < Q; ++a) kz[a] = fma(v, __ldg(zc + a * S), kz[a]);
+                    for (int a = 0; a < Q; ++a) {
+                        double zv[SPL];
+                        ldv<SPL>(zc + a * S, zv);
+#pragma unroll
+                        for (int j = 0; j < SPL; ++j) kz[a][j] = fma(v, zv[j], kz[a][j]);
+                    }
                 }
 #pragma unroll
                 for (int a = 0; a < Q; ++a) {
-                    const double wa = MODE == 1 ? d * zr[a] / omega_n : __ldg(w + base + a * S + k);
-                    z2[a] = zr[a] + omega_n * (wa - kz[a]) / d;
+                    double wv[SPL];
+                    if (MODE == 2) ldv<SPL>(w + base + a * S + k0, wv);
+#pragma unroll
+                    for (int j = 0; j < SPL; ++j) {
+                        const double wa = MODE == 1 ? d * zr[a][j] / omega_n : wv[j];
+                        z2[a][j] = zr[a][j] + omega_n * (wa - kz[a][j]) / d;
+                    }
                 }
             }
         }
-        double u[Q];
+        double u[Q][SPL], sl[SPL];
 #pragma unroll
-        for (int a = 0; a < Q; ++a) {
-            double acc = 0.0;
+        for (int j = 0; j < SPL; ++j) {
 #pragma unroll
-            for (int b = 0; b < Q; ++b) acc += kt.Ctinv[a * Q + b] * z2[b];
-            u[a] = acc;
+            for (int a = 0; a < Q; ++a) {
+                double acc = 0.0;
+#pragma unroll
+                for (int b = 0; b < Q; ++b) acc += kt.Ctinv[a * Q + b] * z2[b][j];
+                u[a][j] = acc;
+            }
+            sl[j] = u[Q - 1][j];
         }
-        const double s = u[Q - 1];
-        double incl = s;
+        double lsum = 0.0;
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) lsum += sl[j];
+        double incl = lsum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const double t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
+            const double tt = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += tt;
         }
-        const double eprev = carry + incl - s;
-        if (valid)
+        double e = carry + incl - lsum;     // end value before this lane's first slab
+        if (valid) {
+            double out[Q][SPL];
 #pragma unroll
-            for (int a = 0; a < Q; ++a) y[base + a * S + k] = u[a] + kt.g[a] * eprev;
+            for (int j = 0; j < SPL; ++j) {
+#pragma unroll
+                for (int a = 0; a < Q; ++a) out[a][j] = u[a][j] + kt.g[a] * e;
+                e += sl[j];
+            }
+#pragma unroll
+            for (int a = 0; a < Q; ++a) stv<SPL>(y + base + a * S + k0, out[a]);
+        }
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (tot && lane == 0) tot[node] = carry;
 }
 
 // x += G y : x[e][a][k] += y[end][a][k] - y[start][a][k]
-template <int Q>
-__global__ void __launch_bounds__(kBlock) k_g_update(int edges, int S, const int *__restrict__ en,
-                                                     const double *__restrict__ y, double *__restrict__ x) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= edges * S) return;
-    const int e = idx / S, k = idx - e * S;
+template <int Q, int SPL>
+__global__ void __launch_bounds__(kBlock) k_g_update(BoxMap m, const int *__restrict__ en, const double *__restrict__ y,
+                                                     double *__restrict__ x) {
+    box_loop(m, [&](int e, int k0, bool valid) {
+    if (!valid) return;
+    const int S = m.S;
     const int n0 = __ldg(en + 2 * e), n1 = __ldg(en + 2 * e + 1);
     const size_t QS = (size_t)Q * S;
 #pragma unroll
-    for (int a = 0; a < Q; ++a)
-        x[(size_t)e * QS + a * S + k] += __ldg(y + n1 * QS + a * S + k) - __ldg(y + n0 * QS + a * S + k);
+    for (int a = 0; a < Q; ++a) {
+        double y0[SPL], y1[SPL], xv[SPL];
+        ldv<SPL>(y + n0 * QS + a * S + k0, y0);
+        ldv<SPL>(y + n1 * QS + a * S + k0, y1);
+        ldv_rw<SPL>(x + e * QS + a * S + k0, xv);
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) xv[j] += y1[j] - y0[j];
+        stv<SPL>(x + e * QS + a * S + k0, xv);
+    }
+});
 }
 
 // ------------------------------------------------------------- transfers
-// fc[rc][a][K] = sum_{(rf,w) in R_s row rc} w * sum_{j,b} Pt_K[(j Q + b)][a] r[rf][b][2K+j]
+// Restriction: fc[rc][a][K] = sum_{(rf,w) in R_s row rc} w * sum_{j,b} Pt_K[(j Q + b)][a] r[rf][b][2K+j]
+// one thread per (coarse row, coarse slab K); the fine slab pair (2K, 2K+1) is one 16-byte load.
 template <int Q, bool SPACE>
-__global__ void __launch_bounds__(kBlock) k_restrict(int crows, int Sc, DevELL Rg, const double *__restrict__ r,
+__global__ void __launch_bounds__(kBlock) k_restrict(Map m, DevELL Rg, const double *__restrict__ r,
                                                      const double *__restrict__ Pt, double *__restrict__ fc) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= crows * Sc) return;
-    const int rc = idx / Sc, K = idx - rc * Sc;
-    const int S = 2 * Sc;
+    int rc, K;
+    if (!map_thread(m, rc, K)) return;
+    const int Sc = m.S, S = 2 * Sc;
     const double *P = Pt + (size_t)K * 2 * Q * Q;
     double acc[Q];
 #pragma unroll
     for (int a = 0; a < Q; ++a) acc[a] = 0.0;
     const int width = SPACE ? Rg.width : 1;
     for (int s = 0; s < width; ++s) {
-        const int rf = SPACE ? __ldg(Rg.col + (size_t)rc * Rg.width + s) : rc;
-        const double wgt = SPACE ? __ldg(Rg.val + (size_t)rc * Rg.width + s) : 1.0;
+        double wgt = 1.0;
+        int rf = rc;
+        if (SPACE) ld_ent(Rg.e + (size_t)rc * Rg.width + s, wgt, rf);
         const double *rr = r + (size_t)rf * Q * S + 2 * K;
         double fv[2 * Q];
 #pragma unroll
-        for (int b = 0; b < Q; ++b) { fv[b] = __ldg(rr + b * S); fv[Q + b] = __ldg(rr + b * S + 1); }
+        for (int b = 0; b < Q; ++b) {
+            const double2 t = __ldg(reinterpret_cast<const double2 *>(rr + b * S));
+            fv[b] = t.x; fv[Q + b] = t.y;
+        }
 #pragma unroll
         for (int a = 0; a < Q; ++a) {
             double t = 0.0;
@@ -392,33 +618,40 @@ __global__ void __launch_bounds__(kBlock) k_restrict(int crows, int Sc, DevELL R
     for (int a = 0; a < Q; ++a) fc[base + a * Sc] = acc[a];
 }
 
-// x[rf][b][k] += sum_a Pt_K[(j Q + b)][a] * sum_{(rc,w) in P_s row rf} w xc[rc][a][K],  K = k/2, j = k%2
+// Prolongation: x[rf][b][2K+j] += sum_a Pt_K[(j Q + b)][a] * sum_{(rc,w) in P_s row rf} w xc[rc][a][K]
+// one thread per (fine row, coarse slab K) writing the fine slab pair as one 16-byte store.
 template <int Q, bool SPACE>
-__global__ void __launch_bounds__(kBlock) k_prolong(int frows, int S, DevELL Pg, const double *__restrict__ xc,
+__global__ void __launch_bounds__(kBlock) k_prolong(Map m, DevELL Pg, const double *__restrict__ xc,
                                                     const double *__restrict__ Pt, double *__restrict__ x) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= frows * S) return;
-    const int rf = idx / S, k = idx - rf * S;
-    const int K = k >> 1, j = k & 1, Sc = S >> 1;
+    int rf, K;
+    if (!map_thread(m, rf, K)) return;
+    const int Sc = m.S, S = 2 * Sc;
     double v[Q];
 #pragma unroll
     for (int a = 0; a < Q; ++a) v[a] = 0.0;
     const int width = SPACE ? Pg.width : 1;
     for (int s = 0; s < width; ++s) {
-        const int rc = SPACE ? __ldg(Pg.col + (size_t)rf * Pg.width + s) : rf;
-        const double wgt = SPACE ? __ldg(Pg.val + (size_t)rf * Pg.width + s) : 1.0;
+        double wgt = 1.0;
+        int rc = rf;
+        if (SPACE) ld_ent(Pg.e + (size_t)rf * Pg.width + s, wgt, rc);
         const double *xr = xc + (size_t)rc * Q * Sc + K;
 #pragma unroll
         for (int a = 0; a < Q; ++a) v[a] = fma(wgt, __ldg(xr + a * Sc), v[a]);
     }
-    const double *P = Pt + (size_t)K * 2 * Q * Q + j * Q * Q;
-    const size_t base = (size_t)rf * Q * S + k;
+    const double *P = Pt + (size_t)K * 2 * Q * Q;
+    const size_t base = (size_t)rf * Q * S + 2 * K;
 #pragma unroll
     for (int b = 0; b < Q; ++b) {
-        double t = 0.0;
+        double t0 = 0.0, t1 = 0.0;
 #pragma unroll
-        for (int a = 0; a < Q; ++a) t += __ldg(P + b * Q + a) * v[a];
-        x[base + b * S] += t;
+        for (int a = 0; a < Q; ++a) {
+            t0 += __ldg(P + b * Q + a) * v[a];
+            t1 += __ldg(P + (Q + b) * Q + a) * v[a];
+        }
+        double2 *px = reinterpret_cast<double2 *>(x + base + b * S);
+        double2 xv = *px;
+        xv.x += t0; xv.y += t1;
+        *px = xv;
     }
 }
 
@@ -437,8 +670,8 @@ __global__ void __launch_bounds__(kBlock) k_coarsest(int n, int S, int k, DevELL
         if (a == 0 && k > 0) {
             double mp = 0.0;
             for (int s = 0; s < M.width; ++s) {
-                const int c = M.col[(size_t)e * M.width + s];
-                mp = fma(M.val[(size_t)e * M.width + s], x[(size_t)c * Q * S + (Q - 1) * S + k - 1], mp);
+                const Ent en = M.e[(size_t)e * M.width + s];
+                mp = fma(en.v, x[(size_t)en.c * Q * S + (Q - 1) * S + k - 1], mp);
             }
             v += mp;
         }
@@ -479,6 +712,43 @@ __global__ void __launch_bounds__(1024) k_reduce(int n, const double *__restrict
 // --------------------------------------------------------------- launchers
 static inline int nblocks(long long work) { return (int)((work + kBlock - 1) / kBlock); }
 
+static Map make_map(int rows, int S, bool allow_pairs = true) {
+    Map m{};
+    m.rows = rows;
+    m.S = S;
+    m.spl = (allow_pairs && S % 2 == 0) ? 2 : 1;
+    const int lanes = (S + m.spl - 1) / m.spl;
+    int l2 = 0;
+    while ((1 << l2) < lanes && l2 < 5) ++l2;
+    m.lpr_log2 = l2;
+    m.rpw = 32 >> l2;
+    m.rows_per_cta = m.rpw * (kBlock / 32);
+    m.n_rowblocks = (rows + m.rows_per_cta - 1) / m.rows_per_cta;
+    m.chunk = (1 << l2) * m.spl;
+    m.n_chunks = (S + m.chunk - 1) / m.chunk;
+    return m;
+}
+static inline int grid(const Map &m) { return m.n_rowblocks * m.n_chunks; }
+
+static BoxMap make_boxmap(int S, const int *sched, const int *bptr, int n_boxes, int max_lpr_log2 = 4) {
+    BoxMap m{};
+    m.S = S;
+    m.spl = S % 2 == 0 ? 2 : 1;
+    const int lanes = (S + m.spl - 1) / m.spl;
+    int l2 = 0;
+    while ((1 << l2) < lanes && l2 < max_lpr_log2) ++l2;
+    m.lpr_log2 = l2;
+    m.rpw = 32 >> l2;
+    m.chunk = (1 << l2) * m.spl;
+    m.n_boxes = n_boxes;
+    m.sched = sched;
+    m.bptr = bptr;
+    return m;
+}
+static inline int grid(const BoxMap &m) { return m.n_boxes * ((m.S + m.chunk - 1) / m.chunk); }
+static inline BoxMap edge_map(const DevLevel &L) { return make_boxmap(L.S, L.sched_e, L.bptr_e, L.nbox_e); }
+static inline BoxMap node_map(const DevLevel &L) { return make_boxmap(L.S, L.sched_n, L.bptr_n, L.nbox_n); }
+
 #define ST_DISPATCH_Q(Q, ...)                                   \
     switch (Q) {                                                \
         case 1: { constexpr int QQ = 1; __VA_ARGS__; } break;   \
@@ -486,34 +756,49 @@ static inline int nblocks(long long work) { return (int)((work + kBlock - 1) / k
         case 3: { constexpr int QQ = 3; __VA_ARGS__; } break;   \
         default: throw std::invalid_argument("Q out of range"); \
     }
+#define ST_DISPATCH_SPL(spl, ...)                               \
+    if (spl == 2) { constexpr int SP = 2; __VA_ARGS__; }        \
+    else { constexpr int SP = 1; __VA_ARGS__; }
+// compile-time ELL widths of the common stencils: uniform hexes (9, 33), general hexes
+// (33, 33), uniform quads (3, 7), general quads (7, 7); anything else runtime
+#define ST_DISPATCH_W(wm, wk, ...)                                                        \
+    if (wm == 9 && wk == 33) { constexpr int WM_ = 9, WK_ = 33; __VA_ARGS__; }           \
+    else if (wm == 33 && wk == 33) { constexpr int WM_ = 33, WK_ = 33; __VA_ARGS__; }    \
+    else if (wm == 3 && wk == 7) { constexpr int WM_ = 3, WK_ = 7; __VA_ARGS__; }        \
+    else if (wm == 7 && wk == 7) { constexpr int WM_ = 7, WK_ = 7; __VA_ARGS__; }        \
+    else { constexpr int WM_ = 0, WK_ = 0; __VA_ARGS__; }
 
 int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
                     const double *prev, double *r, double *z, double omega_s, double *partial) {
-    const int g = nblocks((long long)L.n_edges * L.S);
-    ST_DISPATCH_Q(Q, {
+    const BoxMap m = edge_map(L);
+    const int g = grid(m);
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.K.width, {
         if (partial) {
-            if (r) k_residual<QQ, true, false, true><<<g, kBlock, 0, st>>>(L.n_edges, L.S, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
-            else k_residual<QQ, false, false, true><<<g, kBlock, 0, st>>>(L.n_edges, L.S, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            if (r) k_residual<QQ, SP, WM_, WK_, true, false, true><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            else k_residual<QQ, SP, WM_, WK_, false, false, true><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         } else if (r && z) {
-            k_residual<QQ, true, true, false><<<g, kBlock, 0, st>>>(L.n_edges, L.S, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            k_residual<QQ, SP, WM_, WK_, true, true, false><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         } else if (z) {
-            k_residual<QQ, false, true, false><<<g, kBlock, 0, st>>>(L.n_edges, L.S, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            k_residual<QQ, SP, WM_, WK_, false, true, false><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         } else {
-            k_residual<QQ, true, false, false><<<g, kBlock, 0, st>>>(L.n_edges, L.S, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            k_residual<QQ, SP, WM_, WK_, true, false, false><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         }
-    });
+    })));
     return g;
 }
 
+int residual_partials(const DevLevel &L) { return grid(edge_map(L)); }
+
 void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, bool recon, const double *z,
                   const double *r, double *out, double omega_s, double omega) {
-    const int g = nblocks((long long)L.n_edges * L.S);
-    ST_DISPATCH_Q(Q, {
-        if (last && recon) k_sweep<QQ, true, true><<<g, kBlock, 0, st>>>(L.n_edges, L.S, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
-        else if (last) k_sweep<QQ, true, false><<<g, kBlock, 0, st>>>(L.n_edges, L.S, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
-        else if (recon) k_sweep<QQ, false, true><<<g, kBlock, 0, st>>>(L.n_edges, L.S, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
-        else k_sweep<QQ, false, false><<<g, kBlock, 0, st>>>(L.n_edges, L.S, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
-    });
+    const BoxMap m = edge_map(L);
+    const int g = grid(m);
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.K.width, {
+        if (last && recon) k_sweep<QQ, SP, WM_, WK_, true, true><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+        else if (last) k_sweep<QQ, SP, WM_, WK_, true, false><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+        else if (recon) k_sweep<QQ, SP, WM_, WK_, false, true><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+        else k_sweep<QQ, SP, WM_, WK_, false, false><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+    })));
 }
 
 void launch_axpy(Stream st, size_t n, double alpha, const double *z, double *x) {
@@ -521,47 +806,48 @@ void launch_axpy(Stream st, size_t n, double alpha, const double *z, double *x) 
 }
 
 void launch_gt(Stream st, const DevLevel &L, int Q, const double *r, double omega_n, double *zn, double *w) {
-    const int g = nblocks((long long)L.n_nodes * L.S);
-    ST_DISPATCH_Q(Q, {
-        if (w) k_gt<QQ, true><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.GT, r, L.dN, omega_n, zn, w);
-        else k_gt<QQ, false><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.GT, r, L.dN, omega_n, zn, w);
-    });
+    const BoxMap m = node_map(L);
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, {
+        if (w) k_gt<QQ, SP, true><<<grid(m), kBlock, 0, st>>>(m, L.GT, r, L.dN, omega_n, zn, w);
+        else k_gt<QQ, SP, false><<<grid(m), kBlock, 0, st>>>(m, L.GT, r, L.dN, omega_n, zn, w);
+    }));
 }
 
 void launch_node_sweep(Stream st, const DevLevel &L, int Q, const double *z, const double *w, double omega_n,
                        double *zout) {
-    const int g = nblocks((long long)L.n_nodes * L.S);
-    ST_DISPATCH_Q(Q, k_node_sweep<QQ><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, zout));
+    const BoxMap m = node_map(L);
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, k_node_sweep<QQ, SP><<<grid(m), kBlock, 0, st>>>(m, L.Kn, L.dN, z, w, omega_n, zout)));
 }
 
 void launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mode, const double *z,
                       const double *w, double omega_n, const double *carry, double *y, double *tot) {
     const int g = nblocks((long long)L.n_nodes * 32);
-    ST_DISPATCH_Q(Q, {
-        if (mode == 0) k_node_scan<QQ, 0><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
-        else if (mode == 1) k_node_scan<QQ, 1><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
-        else k_node_scan<QQ, 2><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
-    });
+    const int spl = L.S % 2 == 0 ? 2 : 1;
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(spl, {
+        if (mode == 0) k_node_scan<QQ, SP, 0><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
+        else if (mode == 1) k_node_scan<QQ, SP, 1><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
+        else k_node_scan<QQ, SP, 2><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
+    }));
 }
 
 void launch_g_update(Stream st, const DevLevel &L, int Q, const double *y, double *x) {
-    const int g = nblocks((long long)L.n_edges * L.S);
-    ST_DISPATCH_Q(Q, k_g_update<QQ><<<g, kBlock, 0, st>>>(L.n_edges, L.S, L.edge_nodes, y, x));
+    const BoxMap m = edge_map(L);
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, k_g_update<QQ, SP><<<grid(m), kBlock, 0, st>>>(m, L.edge_nodes, y, x)));
 }
 
 void launch_restrict(Stream st, const DevLevel &F, const DevLevel &C, int Q, const double *r, double *fc) {
-    const int g = nblocks((long long)C.n_edges * C.S);
+    const Map m = make_map(C.n_edges, C.S, false);
     ST_DISPATCH_Q(Q, {
-        if (F.space_coarsened) k_restrict<QQ, true><<<g, kBlock, 0, st>>>(C.n_edges, C.S, F.Rg, r, F.Pt, fc);
-        else k_restrict<QQ, false><<<g, kBlock, 0, st>>>(C.n_edges, C.S, F.Rg, r, F.Pt, fc);
+        if (F.space_coarsened) k_restrict<QQ, true><<<grid(m), kBlock, 0, st>>>(m, F.Rg, r, F.Pt, fc);
+        else k_restrict<QQ, false><<<grid(m), kBlock, 0, st>>>(m, F.Rg, r, F.Pt, fc);
     });
 }
 
 void launch_prolong(Stream st, const DevLevel &F, int Q, const double *xc, double *x) {
-    const int g = nblocks((long long)F.n_edges * F.S);
+    const Map m = make_map(F.n_edges, F.S / 2, false);
     ST_DISPATCH_Q(Q, {
-        if (F.space_coarsened) k_prolong<QQ, true><<<g, kBlock, 0, st>>>(F.n_edges, F.S, F.Pg, xc, F.Pt, x);
-        else k_prolong<QQ, false><<<g, kBlock, 0, st>>>(F.n_edges, F.S, F.Pg, xc, F.Pt, x);
+        if (F.space_coarsened) k_prolong<QQ, true><<<grid(m), kBlock, 0, st>>>(m, F.Pg, xc, F.Pt, x);
+        else k_prolong<QQ, false><<<grid(m), kBlock, 0, st>>>(m, F.Pg, xc, F.Pt, x);
     });
 }
 

@@ -514,6 +514,33 @@ static double level_lambda(const HostLevel &L) {
     return lam;
 }
 
+// Row schedules for L1 reuse: the rows of a small box of nodes
+// (3D 4x2x2, 2D 8x4) are processed by one CTA, so the columns they share are
+// fetched from L2 once per CTA.  Edge (dir, node) belongs to the box of its
+// start node; within a box: node order, then direction.
+static void box_schedule(const HostMesh &m, HostLevel &L) {
+    const int d = m.dim;
+    const int B[3] = {d == 3 ? 4 : 8, d == 3 ? 2 : 4, d == 3 ? 2 : 1};
+    const int nn[3] = {m.n[0] + 1, m.n[1] + 1, d == 3 ? m.n[2] + 1 : 1};
+    const int nb[3] = {(nn[0] + B[0] - 1) / B[0], (nn[1] + B[1] - 1) / B[1], (nn[2] + B[2] - 1) / B[2]};
+    L.sched_e.clear(); L.bptr_e.assign(1, 0); L.sched_n.clear(); L.bptr_n.assign(1, 0);
+    const int nx = m.n[0], ny = m.n[1], nz = d == 3 ? m.n[2] : 0;
+    for (int bk = 0; bk < nb[2]; ++bk)
+        for (int bj = 0; bj < nb[1]; ++bj)
+            for (int bi = 0; bi < nb[0]; ++bi) {
+                for (int k = bk * B[2]; k < std::min(nn[2], (bk + 1) * B[2]); ++k)
+                    for (int j = bj * B[1]; j < std::min(nn[1], (bj + 1) * B[1]); ++j)
+                        for (int i = bi * B[0]; i < std::min(nn[0], (bi + 1) * B[0]); ++i) {
+                            L.sched_n.push_back(i + (nx + 1) * (j + (ny + 1) * k));
+                            if (i < nx) L.sched_e.push_back(i + nx * (j + (ny + 1) * k));
+                            if (j < ny) L.sched_e.push_back(m.Ex + i + (nx + 1) * (j + ny * k));
+                            if (d == 3 && k < nz) L.sched_e.push_back(m.Ex + m.Ey + i + (nx + 1) * (j + (ny + 1) * k));
+                        }
+                L.bptr_e.push_back((int)L.sched_e.size());
+                L.bptr_n.push_back((int)L.sched_n.size());
+            }
+}
+
 void build_hierarchy(const st_params &p, const Options &o, const TimeMats &tm, std::vector<HostLevel> &levels) {
     const int Q = tm.Q, q = Q - 1;
     levels.clear();
@@ -531,6 +558,7 @@ void build_hierarchy(const st_params &p, const Options &o, const TimeMats &tm, s
     for (int lvl = 0;; ++lvl) {
         HostLevel &L = levels[lvl];
         assemble(L);
+        box_schedule(L.mesh, L);
         const int S = (int)L.tau.size();
         L.lambda = level_lambda(L);
         if (S <= o.min_slabs || S % 2) break;
