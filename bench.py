@@ -232,6 +232,7 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args), "rhs": "U(-1,1) drawn on the device (torch generator, seed 3)", "n_edges": s.n_edges, "slabs_per_gpu": args.slabs,
                    "dofs_per_gpu": n_dofs, "levels": info["n_levels"],
+                   "matrix_free_levels": sum(info["level_matrix_free"]),
                    "l2": f"no flush: every space-time vector is {8 * n_dofs / 1e9:.2f} GB >> 126 MB L2",
                    "parallelism": f"slab blocks, {world} replica(s)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -70,6 +70,8 @@ typedef struct st_params {
     double lambda_crit;    /* Eq. (3) threshold, default 0.1 (l.292) */
     int mode;              /* 0 auto (Eq. 3 per level), 1 semi-time only, 2 full at the top level only (Table 1) */
     int min_slabs;         /* stop time coarsening at this many slabs, default 1 */
+    int kernel_path;       /* 0: matrix-free pencil march on uniform hex levels, ELL elsewhere
+                              (default); 1: assembled ELL operators everywhere */
 } st_params;
 
 typedef struct st_info_t {
@@ -81,6 +83,7 @@ typedef struct st_info_t {
     double level_lambda[32];        /* Eq. (3) lambda of level l (min over cells) */
     int64_t kernel_launches;        /* kernels launched by this handle so far */
     int64_t device_bytes;           /* bytes of device memory the handle owns */
+    int level_matrix_free[32];      /* 1 if level l runs the matrix-free pencil march */
 } st_info_t;
 
 /* Build the level hierarchy (mesh coarsening by Eq. 3, operators, transfers,

@@ -7,6 +7,7 @@ fallback: if libst.so is missing or no CUDA device is present, calls raise.
 """
 import ctypes
 import os
+import sys
 
 import numpy as np
 
@@ -25,7 +26,8 @@ class StParams(ctypes.Structure):
                 ("tau", ctypes.POINTER(ctypes.c_double)), ("n_slabs", ctypes.c_int), ("q", ctypes.c_int),
                 ("spec", ctypes.c_char_p), ("omega", ctypes.c_double), ("nu_s", ctypes.c_int),
                 ("omega_s", ctypes.c_double), ("nu_n", ctypes.c_int), ("omega_n", ctypes.c_double),
-                ("lambda_crit", ctypes.c_double), ("mode", ctypes.c_int), ("min_slabs", ctypes.c_int)]
+                ("lambda_crit", ctypes.c_double), ("mode", ctypes.c_int), ("min_slabs", ctypes.c_int),
+                ("kernel_path", ctypes.c_int)]
 
 
 class StInfo(ctypes.Structure):
@@ -33,7 +35,7 @@ class StInfo(ctypes.Structure):
                 ("level_n_edges", ctypes.c_int * 32), ("level_n_nodes", ctypes.c_int * 32),
                 ("level_n_slabs", ctypes.c_int * 32), ("level_space_coarsened", ctypes.c_int * 32),
                 ("level_lambda", ctypes.c_double * 32), ("kernel_launches", ctypes.c_int64),
-                ("device_bytes", ctypes.c_int64)]
+                ("device_bytes", ctypes.c_int64), ("level_matrix_free", ctypes.c_int * 32)]
 
 
 class StKstat(ctypes.Structure):
@@ -86,7 +88,7 @@ def _dptr(a):
 
 
 def make_params(dim, n, sigma, nu, tau, q=1, coords=None, spec="SAS", omega=0.5, nu_s=2, omega_s=None,
-                nu_n=2, omega_n=0.6, lambda_crit=0.1, mode=0, min_slabs=1):
+                nu_n=2, omega_n=0.6, lambda_crit=0.1, mode=0, min_slabs=1, kernel_path=0):
     """Fill an StParams; returns (params, keep-alive list)."""
     keep = [np.ascontiguousarray(sigma, dtype=np.float64), np.ascontiguousarray(nu, dtype=np.float64),
             np.ascontiguousarray(tau, dtype=np.float64), spec.encode()]
@@ -105,6 +107,7 @@ def make_params(dim, n, sigma, nu, tau, q=1, coords=None, spec="SAS", omega=0.5,
     p.omega, p.nu_s, p.nu_n, p.omega_n = omega, nu_s, nu_n, omega_n
     p.omega_s = omega_s if omega_s is not None else (0.6 if dim == 3 else 0.5)
     p.lambda_crit, p.mode, p.min_slabs = lambda_crit, mode, min_slabs
+    p.kernel_path = kernel_path
     return p, keep
 
 
@@ -115,7 +118,8 @@ def _info_dict(inf):
             "level_n_slabs": list(inf.level_n_slabs[:L]),
             "level_space_coarsened": list(inf.level_space_coarsened[:L]),
             "level_lambda": list(inf.level_lambda[:L]),
-            "kernel_launches": inf.kernel_launches, "device_bytes": inf.device_bytes}
+            "kernel_launches": inf.kernel_launches, "device_bytes": inf.device_bytes,
+            "level_matrix_free": list(inf.level_matrix_free[:L])}
 
 
 def plan(*args, **kw):
@@ -143,14 +147,14 @@ class Solver:
     """Handle over st_setup for one workload (see workloads.Workload for the fields)."""
 
     def __init__(self, dim, n, sigma, nu, tau, q=1, coords=None, spec="SAS", omega=0.5, nu_s=2, omega_s=None,
-                 nu_n=2, omega_n=0.6, lambda_crit=0.1, mode=0, min_slabs=1, stream=None):
+                 nu_n=2, omega_n=0.6, lambda_crit=0.1, mode=0, min_slabs=1, kernel_path=0, stream=None):
         import torch
         if not torch.cuda.is_available():
             raise StError("no CUDA device: the space-time multigrid has no CPU path")
         lib = load()
         p, self._keep = make_params(dim, n, sigma, nu, tau, q=q, coords=coords, spec=spec, omega=omega, nu_s=nu_s,
                                     omega_s=omega_s, nu_n=nu_n, omega_n=omega_n, lambda_crit=lambda_crit, mode=mode,
-                                    min_slabs=min_slabs)
+                                    min_slabs=min_slabs, kernel_path=kernel_path)
         self.dim, self.n, self.q, self.S = dim, tuple(n), q, p.n_slabs
         h = ctypes.c_void_p()
         _check(lib.st_setup(ctypes.byref(p), ctypes.byref(h)))
@@ -175,8 +179,7 @@ class Solver:
             self._h = None
 
     def __del__(self):
-        import sys
-        if sys.is_finalizing():
+        if sys is None or sys.is_finalizing():
             return          # the CUDA context may already be gone; the process exit frees everything
         try:
             self.close()

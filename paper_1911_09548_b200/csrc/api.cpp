@@ -273,6 +273,8 @@ static void parse_options(const st_params *p, st::Options &o) {
     if (p->mode < 0 || p->mode > 2) throw std::invalid_argument("mode must be 0, 1 or 2");
     o.mode = p->mode;
     if (p->min_slabs > 0) o.min_slabs = p->min_slabs;
+    if (p->kernel_path < 0 || p->kernel_path > 1) throw std::invalid_argument("kernel_path must be 0 or 1");
+    o.kernel_path = p->kernel_path;
 }
 
 const char *st_last_error(void) { return g_err.c_str(); }
@@ -307,6 +309,16 @@ int st_setup(const st_params *p, st_handle **out) {
             D.nbox_e = (int)H.bptr_e.size() - 1; D.nbox_n = (int)H.bptr_n.size() - 1;
             D.tau = h->upload(H.tau);
             D.space_coarsened = H.space_coarsened;
+            if (H.uniform && o.kernel_path == 0) {
+                const double hx = H.hbox[0], hy = H.hbox[1], hz = H.hbox[2];
+                D.use_march = true;
+                D.grid.nx = H.mesh.n[0]; D.grid.ny = H.mesh.n[1]; D.grid.nz = H.mesh.n[2];
+                D.grid.Ex = H.mesh.Ex; D.grid.Ey = H.mesh.Ey;
+                D.grid.mx = hy * hz / hx; D.grid.my = hx * hz / hy; D.grid.mz = hx * hy / hz;
+                D.grid.wx = hx / (hy * hz); D.grid.wy = hy / (hx * hz); D.grid.wz = hz / (hx * hy);
+                D.grid.sigma = h->upload(H.sigma);
+                D.grid.nu = h->upload(H.nu);
+            }
             const bool coarsest = l + 1 == h->hl.size();
             if (!coarsest) {
                 D.Pt = h->upload(H.Pt);
@@ -516,6 +528,7 @@ int st_info(const st_handle *h, st_info_t *info) {
         info->level_space_coarsened[l] = h->hl[l].space_coarsened ? 1 : 0;
         info->level_lambda[l] = h->hl[l].lambda;
     }
+    for (int l = 0; l < info->n_levels; ++l) info->level_matrix_free[l] = h->dl[l].use_march ? 1 : 0;
     info->kernel_launches = h->launches;
     info->device_bytes = h->bytes;
     return 0;

@@ -64,6 +64,16 @@ struct HostLevel {
     std::vector<double> Ainv;                   // coarsest only: per slab dense (QN x QN)
     // box schedules: rows ordered by small node boxes (box b = rows sched[bptr[b] .. bptr[b+1]))
     std::vector<int> sched_e, bptr_e, sched_n, bptr_n;
+    bool uniform = false;                       // all cells the same axis-aligned box
+    double hbox[3] = {0, 0, 0};
+};
+
+// uniform axis-aligned hex level for the matrix-free pencil march (march.cuh)
+struct Grid3 {
+    int nx, ny, nz, Ex, Ey;
+    double mx, my, mz;
+    double wx, wy, wz;
+    const double *sigma, *nu;
 };
 
 struct DevLevel {
@@ -73,6 +83,8 @@ struct DevLevel {
     int *edge_nodes = nullptr;
     int *sched_e = nullptr, *bptr_e = nullptr, *sched_n = nullptr, *bptr_n = nullptr;
     int nbox_e = 0, nbox_n = 0;
+    bool use_march = false;
+    Grid3 grid{};
     double *tau = nullptr;
     double *Pt = nullptr;
     double *Ainv = nullptr;
@@ -93,6 +105,7 @@ struct Options {
     double lambda_crit = 0.1;
     int mode = 0;
     int min_slabs = 1;
+    int kernel_path = 0;    // 0: matrix-free march on uniform hex levels, ELL elsewhere; 1: ELL only
 };
 
 // kernel-side time constants (passed by value to kernels)

@@ -19,6 +19,7 @@
 #include <stdexcept>
 
 #include "internal.h"
+#include "march.cuh"
 
 namespace st {
 
@@ -580,6 +581,162 @@ __global__ void __launch_bounds__(kBlock) k_g_update(BoxMap m, const int *__rest
 });
 }
 
+
+// ------------------------------------------------ pencil march (uniform hex levels)
+// Grid: blocks ordered slab-chunk-major; block = 4 warps = 4 consecutive pencils (j, k)
+// of one slab chunk.  HALO (residual): lane 0 is the slab before the chunk so that its
+// mass image of time node q feeds lane 1's upwind coupling by a shuffle; chunk stride 31.
+struct MarchMap {
+    int S, n_pencils, n_pblocks, stride;
+};
+constexpr int kMarchWarps = 4;
+
+template <bool HALO>
+__device__ __forceinline__ void march_coords(const MarchMap &mm, const Grid3 &g, int &j, int &k, int &ks, bool &out_ok,
+                                             bool &pencil_ok) {
+    const int chunk = blockIdx.x / mm.n_pblocks;
+    const int pb = blockIdx.x - chunk * mm.n_pblocks;
+    const int p = pb * kMarchWarps + (threadIdx.x >> 5);
+    pencil_ok = p < mm.n_pencils;
+    const int pp = pencil_ok ? p : 0;
+    j = pp % (g.ny + 1);
+    k = pp / (g.ny + 1);
+    const int lane = threadIdx.x & 31;
+    ks = HALO ? chunk * 31 + lane - 1 : chunk * 32 + lane;
+    out_ok = (HALO ? lane >= 1 : true) && ks < mm.S;
+    if (ks >= mm.S) ks = mm.S - 1;
+}
+
+template <int Q, bool R_OUT, bool Z_OUT, bool NORM>
+__global__ void __launch_bounds__(32 * kMarchWarps) k_res_march(MarchMap mm, Grid3 g, const double *__restrict__ tau,
+                                                                const double *__restrict__ x,
+                                                                const double *__restrict__ f,
+                                                                const double *__restrict__ prev, double *__restrict__ r,
+                                                                double *__restrict__ z, const double *__restrict__ dM,
+                                                                const double *__restrict__ dK, double omega_s, KT kt,
+                                                                double *__restrict__ partial) {
+    int j, k, ks;
+    bool out_ok, pencil_ok;
+    march_coords<true>(mm, g, j, k, ks, out_ok, pencil_ok);
+    double nrm = 0.0;
+    if (pencil_ok) {
+        const int S = mm.S, QS = Q * S;
+        const Lane ln{x, prev, S, QS, ks, Q - 1};
+        const double t = ks >= 0 ? __ldg(tau + ks) : 0.0;
+        Win w[Q];
+#pragma unroll
+        for (int a = 0; a < Q; ++a) win_init(g, ln, a, j, k, w[a]);
+        Cells c;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { (&c.s[0][0][0])[u] = 0.0; (&c.n[0][0][0])[u] = 0.0; }
+        for (int i = 0; i <= g.nx; ++i) {
+            load_cells(g, i, j, k, c);
+            double o[Q][6];
+#pragma unroll
+            for (int a = 0; a < Q; ++a) step(g, ln, c, a, i, j, k, w[a], o[a]);
+#pragma unroll
+            for (int e = 0; e < 3; ++e) {
+                const bool exists = e == 0 ? i < g.nx : (e == 1 ? j < g.ny : k < g.nz);   // warp-uniform
+                if (!exists) continue;
+                const double mp = __shfl_up_sync(0xffffffffu, o[Q - 1][e], 1);
+                const int row = e == 0 ? xid(g, i, j, k) : (e == 1 ? yid(g, i, j, k) : zid(g, i, j, k));
+                if (!out_ok) continue;
+                const size_t base = (size_t)row * QS + ks;
+                double rr[Q];
+#pragma unroll
+                for (int b = 0; b < Q; ++b) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int a = 0; a < Q; ++a) acc += kt.Ct[b * Q + a] * o[a][e] + t * kt.Mt[b * Q + a] * o[a][3 + e];
+                    rr[b] = __ldg(f + base + b * S) - acc + (b == 0 ? mp : 0.0);
+                }
+                if (R_OUT)
+#pragma unroll
+                    for (int b = 0; b < Q; ++b) r[base + b * S] = rr[b];
+                if (Z_OUT) {
+                    double y[Q];
+                    block_solve<Q>(kt, __ldg(dM + row), __ldg(dK + row), t, rr, y);
+#pragma unroll
+                    for (int b = 0; b < Q; ++b) z[base + b * S] = omega_s * y[b];
+                }
+                if (NORM)
+#pragma unroll
+                    for (int b = 0; b < Q; ++b) nrm += rr[b] * rr[b];
+            }
+        }
+    }
+    if (NORM) {
+        __shared__ double sh[kMarchWarps];
+        const double s = block_reduce_sum(nrm, sh);
+        if (threadIdx.x == 0) partial[blockIdx.x] = s;
+    }
+}
+
+// Jacobi sweep on A_k with the march: znew = z + omega_s D^{-1}(r - A_k z), r = D z / omega_s
+// (RECON) or read; LAST: x += omega znew, else out = znew.
+template <int Q, bool LAST, bool RECON>
+__global__ void __launch_bounds__(32 * kMarchWarps) k_sweep_march(MarchMap mm, Grid3 g, const double *__restrict__ tau,
+                                                                  const double *__restrict__ dM,
+                                                                  const double *__restrict__ dK,
+                                                                  const double *__restrict__ z,
+                                                                  const double *__restrict__ r, double *out,
+                                                                  double omega_s, double omega, KT kt) {
+    int j, k, ks;
+    bool out_ok, pencil_ok;
+    march_coords<false>(mm, g, j, k, ks, out_ok, pencil_ok);
+    if (!pencil_ok) return;
+    const int S = mm.S, QS = Q * S;
+    const Lane ln{z, nullptr, S, QS, ks, Q - 1};
+    const double t = __ldg(tau + ks);
+    Win w[Q];
+#pragma unroll
+    for (int a = 0; a < Q; ++a) win_init(g, ln, a, j, k, w[a]);
+    Cells c;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) { (&c.s[0][0][0])[u] = 0.0; (&c.n[0][0][0])[u] = 0.0; }
+    for (int i = 0; i <= g.nx; ++i) {
+        load_cells(g, i, j, k, c);
+        double o[Q][6];
+#pragma unroll
+        for (int a = 0; a < Q; ++a) step(g, ln, c, a, i, j, k, w[a], o[a]);
+        if (!out_ok) continue;
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            const bool exists = e == 0 ? i < g.nx : (e == 1 ? j < g.ny : k < g.nz);
+            if (!exists) continue;
+            const int row = e == 0 ? xid(g, i, j, k) : (e == 1 ? yid(g, i, j, k) : zid(g, i, j, k));
+            const size_t base = (size_t)row * QS + ks;
+            const double dm = __ldg(dM + row), dk = __ldg(dK + row);
+            double zr[Q], rv[Q], d[Q], y[Q];
+#pragma unroll
+            for (int a = 0; a < Q; ++a) zr[a] = z[base + a * S];
+            if (RECON) {
+                block_mul<Q>(kt, dm, dk, t, zr, rv);
+#pragma unroll
+                for (int a = 0; a < Q; ++a) rv[a] /= omega_s;
+            } else {
+#pragma unroll
+                for (int a = 0; a < Q; ++a) rv[a] = __ldg(r + base + a * S);
+            }
+#pragma unroll
+            for (int b = 0; b < Q; ++b) {
+                double acc = 0.0;
+#pragma unroll
+                for (int a = 0; a < Q; ++a) acc += kt.Ct[b * Q + a] * o[a][e] + t * kt.Mt[b * Q + a] * o[a][3 + e];
+                d[b] = rv[b] - acc;
+            }
+            block_solve<Q>(kt, dm, dk, t, d, y);
+            if (LAST) {
+#pragma unroll
+                for (int a = 0; a < Q; ++a) out[base + a * S] += omega * (zr[a] + omega_s * y[a]);
+            } else {
+#pragma unroll
+                for (int a = 0; a < Q; ++a) out[base + a * S] = zr[a] + omega_s * y[a];
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------- transfers
 // Restriction: fc[rc][a][K] = sum_{(rf,w) in R_s row rc} w * sum_{j,b} Pt_K[(j Q + b)][a] r[rf][b][2K+j]
 // one thread per (coarse row, coarse slab K); the fine slab pair (2K, 2K+1) is one 16-byte load.
@@ -768,8 +925,36 @@ static inline BoxMap node_map(const DevLevel &L) { return make_boxmap(L.S, L.sch
     else if (wm == 7 && wk == 7) { constexpr int WM_ = 7, WK_ = 7; __VA_ARGS__; }        \
     else { constexpr int WM_ = 0, WK_ = 0; __VA_ARGS__; }
 
+static MarchMap march_map(const DevLevel &L, bool halo) {
+    MarchMap mm{};
+    mm.S = L.S;
+    mm.n_pencils = (L.grid.ny + 1) * (L.grid.nz + 1);
+    mm.n_pblocks = (mm.n_pencils + kMarchWarps - 1) / kMarchWarps;
+    mm.stride = halo ? 31 : 32;
+    return mm;
+}
+static inline int grid(const MarchMap &mm) { return mm.n_pblocks * ((mm.S + mm.stride - 1) / mm.stride); }
+
 int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
                     const double *prev, double *r, double *z, double omega_s, double *partial) {
+    if (L.use_march) {
+        const MarchMap mm = march_map(L, true);
+        const int g = grid(mm);
+        const int nt = 32 * kMarchWarps;
+        ST_DISPATCH_Q(Q, {
+            if (partial) {
+                if (r) k_res_march<QQ, true, false, true><<<g, nt, 0, st>>>(mm, L.grid, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+                else k_res_march<QQ, false, false, true><<<g, nt, 0, st>>>(mm, L.grid, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            } else if (r && z) {
+                k_res_march<QQ, true, true, false><<<g, nt, 0, st>>>(mm, L.grid, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            } else if (z) {
+                k_res_march<QQ, false, true, false><<<g, nt, 0, st>>>(mm, L.grid, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            } else {
+                k_res_march<QQ, true, false, false><<<g, nt, 0, st>>>(mm, L.grid, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            }
+        });
+        return g;
+    }
     const BoxMap m = edge_map(L);
     const int g = grid(m);
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.K.width, {
@@ -787,10 +972,23 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
     return g;
 }
 
-int residual_partials(const DevLevel &L) { return grid(edge_map(L)); }
+int residual_partials(const DevLevel &L) {
+    return L.use_march ? grid(march_map(L, true)) : grid(edge_map(L));
+}
 
 void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, bool recon, const double *z,
                   const double *r, double *out, double omega_s, double omega) {
+    if (L.use_march) {
+        const MarchMap mm = march_map(L, false);
+        const int g = grid(mm), nt = 32 * kMarchWarps;
+        ST_DISPATCH_Q(Q, {
+            if (last && recon) k_sweep_march<QQ, true, true><<<g, nt, 0, st>>>(mm, L.grid, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+            else if (last) k_sweep_march<QQ, true, false><<<g, nt, 0, st>>>(mm, L.grid, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+            else if (recon) k_sweep_march<QQ, false, true><<<g, nt, 0, st>>>(mm, L.grid, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+            else k_sweep_march<QQ, false, false><<<g, nt, 0, st>>>(mm, L.grid, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+        });
+        return;
+    }
     const BoxMap m = edge_map(L);
     const int g = grid(m);
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.K.width, {

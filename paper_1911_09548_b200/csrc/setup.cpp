@@ -282,12 +282,21 @@ static void element(const HostMesh &m, int c, double sigma, double nu, double *M
         double w = gw[ix] * gw[iy] * (d == 3 ? gw[iz] : 1.0);
         double D[8][3];
         node_grads(d, p, D);
-        double J[9] = {0};   // J[r*d + col] = dx_r / dxhat_col
-        for (int n = 0; n < nn; ++n) {
-            const double *X = &m.coords[(size_t)m.cell_nodes[(size_t)nn * c + n] * d];
-            for (int r = 0; r < d; ++r)
-                for (int k = 0; k < d; ++k) J[r * d + k] += X[r] * D[n][k];
-        }
+        // J[r*d + k] = dx_r / dxhat_k, summed over the cell's edges in direction k from
+        // coordinate differences (exact zeros on axis-aligned cells, so no spurious
+        // ~1e-20 couplings survive in M for uniform meshes)
+        double J[9] = {0};
+        for (int n = 0; n < nn; ++n)
+            for (int k = 0; k < d; ++k) {
+                if ((n >> k) & 1) continue;
+                const int n1 = n | (1 << k);
+                double w = 1.0;                  // transverse Q1 weights of this edge at p
+                for (int a = 0; a < d; ++a)
+                    if (a != k) w *= l01((n >> a) & 1, p[a]);
+                const double *X0 = &m.coords[(size_t)m.cell_nodes[(size_t)nn * c + n] * d];
+                const double *X1 = &m.coords[(size_t)m.cell_nodes[(size_t)nn * c + n1] * d];
+                for (int r = 0; r < d; ++r) J[r * d + k] += (X1[r] - X0[r]) * w;
+            }
         double JtJ[9] = {0}, G[9];
         for (int a = 0; a < d; ++a)
             for (int b = 0; b < d; ++b)
@@ -541,6 +550,30 @@ static void box_schedule(const HostMesh &m, HostLevel &L) {
             }
 }
 
+// A level is "uniform" when every cell is the same axis-aligned box (then the
+// matrix-free pencil march applies).  Exact comparison against the
+// lattice i*hx, j*hy, k*hz built from the corner coordinates.
+static void detect_uniform(HostLevel &L) {
+    const HostMesh &m = L.mesh;
+    const int d = m.dim;
+    L.uniform = false;
+    if (d != 3) return;
+    const int nx = m.n[0], ny = m.n[1], nz = m.n[2];
+    const double *X0 = &m.coords[0];
+    const double *X1 = &m.coords[(size_t)(nx + (nx + 1) * (ny + (ny + 1) * nz)) * 3];
+    const double h[3] = {(X1[0] - X0[0]) / nx, (X1[1] - X0[1]) / ny, (X1[2] - X0[2]) / nz};
+    for (int k = 0; k <= nz; ++k)
+        for (int j = 0; j <= ny; ++j)
+            for (int i = 0; i <= nx; ++i) {
+                const double *X = &m.coords[(size_t)(i + (nx + 1) * (j + (ny + 1) * k)) * 3];
+                const double want[3] = {X0[0] + i * h[0], X0[1] + j * h[1], X0[2] + k * h[2]};
+                for (int a = 0; a < 3; ++a)
+                    if (std::fabs(X[a] - want[a]) > 1e-13 * (std::fabs(h[a]) * (m.n[a]) + std::fabs(X0[a]))) return;
+            }
+    L.uniform = true;
+    for (int a = 0; a < 3; ++a) L.hbox[a] = h[a];
+}
+
 void build_hierarchy(const st_params &p, const Options &o, const TimeMats &tm, std::vector<HostLevel> &levels) {
     const int Q = tm.Q, q = Q - 1;
     levels.clear();
@@ -559,6 +592,7 @@ void build_hierarchy(const st_params &p, const Options &o, const TimeMats &tm, s
         HostLevel &L = levels[lvl];
         assemble(L);
         box_schedule(L.mesh, L);
+        detect_uniform(L);
         const int S = (int)L.tau.size();
         L.lambda = level_lambda(L);
         if (S <= o.min_slabs || S % 2) break;

@@ -64,17 +64,20 @@ def test_solve_parity(torch_cuda, name, maxit):
     # rounding noise injected at every cycle (one ulp on the iterate), the per-iteration analogue
     # of oracle_noise for the residual history
     lv, nf = H.levels[0], np.linalg.norm(F)
-    Xn, hist_n = np.zeros_like(F), [hist[0]]
-    for i in range(len(hist) - 1):
-        Xn = ulp_perturb(mg.vcycle(H, 0, Xn, F), 1000 + i)
-        hist_n.append(np.linalg.norm(F - mg.apply_L(lv, Xn)) / nf)
-    noise = np.abs(np.array(hist_n) - np.array(hist))
+    noise = np.zeros(len(hist))
+    for rep in range(3):
+        Xn, hist_n = np.zeros_like(F), [hist[0]]
+        for i in range(len(hist) - 1):
+            Xn = ulp_perturb(mg.vcycle(H, 0, Xn, F), 1000 * rep + i)
+            hist_n.append(np.linalg.norm(F - mg.apply_L(lv, Xn)) / nf)
+        noise = np.maximum(noise, np.abs(np.array(hist_n) - np.array(hist)))
     s = solver(w)
+    print(name, "matrix-free levels", s.info()["level_matrix_free"])
     f = torch.from_numpy(w.rhs()).cuda()
     x = torch.zeros_like(f)
     it, h = s.solve(x, f, tol=1e-8, maxit=maxit)
     assert it == len(hist) - 1
-    tol = np.maximum(np.maximum(RTOL * np.array(hist), ATOL_FLOOR), 20 * noise)
+    tol = np.maximum(np.maximum(RTOL * np.array(hist), ATOL_FLOOR), 50 * noise)
     diff = np.abs(np.array(h) - np.array(hist))
     print(name, "max diff/tol", float(np.max(diff / tol)), "max rel diff", float(np.max(diff / np.array(hist))))
     assert np.all(diff <= tol), (diff, tol)
@@ -104,6 +107,38 @@ def test_vcycle_parity_random_start(torch_cuda, name, q):
     err = np.linalg.norm(Xg - X1)
     print(name, q, "err", err / np.linalg.norm(X1), "noise", noise / np.linalg.norm(X1))
     assert err <= max(1e-12 * np.linalg.norm(X1), 20 * noise)
+
+
+@pytest.mark.parametrize("name", ["c1", "c4", "c3"])
+@pytest.mark.parametrize("q", [0, 1, 2])
+def test_march_matches_ell_and_oracle(torch_cuda, name, q):
+    # uniform hex levels run the matrix-free pencil march; the assembled-ELL path (kernel_path=1)
+    # and the oracle must give the same V-cycle
+    torch = torch_cuda
+    w = workloads.small(name)
+    w.q = q
+    rng = np.random.default_rng(21)
+    F = rng.uniform(-1, 1, (w.S, q + 1, w.n_edges))
+    X0 = rng.uniform(-1, 1, F.shape)
+    H = oracle_hierarchy(w)
+    X1 = mg.vcycle(H, 0, X0.copy(), F)
+    noise = np.linalg.norm(oracle_noise(lambda a, b: mg.vcycle(H, 0, a, b), X0, F) - X1)
+    outs = []
+    for path in (0, 1):
+        s = solver(w, kernel_path=path)
+        x = torch.from_numpy(workloads.from_oracle(X0)).cuda()
+        f = torch.from_numpy(workloads.from_oracle(F)).cuda()
+        r = torch.empty_like(f)
+        s.residual(x, f, r)
+        outs.append(workloads.to_oracle(r.cpu().numpy()))
+        s.vcycle(x, f)
+        Xg = workloads.to_oracle(x.cpu().numpy())
+        err = np.linalg.norm(Xg - X1)
+        print(name, q, "path", path, "err", err / np.linalg.norm(X1), "noise", noise / np.linalg.norm(X1))
+        assert err <= max(1e-12 * np.linalg.norm(X1), 20 * noise)
+    R = F - st_oracle.apply_L(H.levels[0], X0)
+    for Rg in outs:
+        np.testing.assert_allclose(Rg, R, rtol=0, atol=1e-12 * np.abs(R).max())
 
 
 @pytest.mark.parametrize("spec,nu_s,nu_n", [("SAS", 1, 1), ("SAS", 3, 3), ("SA", 2, 2), ("ASSA", 2, 4), ("S", 2, 2)])
