@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -68,8 +69,17 @@ struct st_handle {
         return e;
     }
     // run `launch` (which issues exactly `count` kernels) and, when profiling, time it
+    bool debug_sync = false;   // env ST_DEBUG_SYNC=1: synchronise and check after every launch
     template <class F>
     void run(const char *fam, double bytes, int count, F &&launch) {
+        if (debug_sync) {
+            launch();
+            launches += count;
+            cudaError_t e = cudaStreamSynchronize(stream);
+            if (e == cudaSuccess) e = cudaGetLastError();
+            if (e != cudaSuccess) throw CudaError(std::string("kernel ") + fam + ": " + cudaGetErrorString(e));
+            return;
+        }
         if (!prof) { launch(); launches += count; return; }
         Rec r{fam_id(fam), bytes, ev(), ev()};
         ck(cudaEventRecord(r.a, stream), "event record");
@@ -203,9 +213,10 @@ void vcycle(st_handle *h, int l, double *x, const double *f) {
 double residual_norm2(st_handle *h, const double *x, const double *f) {
     DevLevel &L = h->dl[0];
     auto s = (st::Stream)h->stream;
-    int g = st::launch_residual(s, L, h->kt, h->Q, x, f, nullptr, nullptr, nullptr, h->o.omega_s, h->partial);
-    st::launch_reduce(s, g, h->partial, h->dscal);
-    h->launches += 2;
+    int g = 0;
+    h->run("residual_norm", 2 * evec(L, h->Q) + op_bytes(L), 1,
+           [&] { g = st::launch_residual(s, L, h->kt, h->Q, x, f, nullptr, nullptr, nullptr, h->o.omega_s, h->partial); });
+    h->run("reduce", 8.0 * g, 1, [&] { st::launch_reduce(s, g, h->partial, h->dscal); });
     double v = 0;
     ck(cudaMemcpyAsync(&v, h->dscal, sizeof(double), cudaMemcpyDeviceToHost, h->stream), "norm d2h");
     ck(cudaStreamSynchronize(h->stream), "sync");
@@ -215,9 +226,9 @@ double residual_norm2(st_handle *h, const double *x, const double *f) {
 double norm2_plain(st_handle *h, const double *v, size_t n) {
     // ||v||^2 via the residual kernel would need x = 0; use a dedicated pass instead
     auto s = (st::Stream)h->stream;
-    int g = st::launch_norm2(s, n, v, h->partial);
-    st::launch_reduce(s, g, h->partial, h->dscal);
-    h->launches += 2;
+    int g = 0;
+    h->run("norm2", 8.0 * n, 1, [&] { g = st::launch_norm2(s, n, v, h->partial); });
+    h->run("reduce", 8.0 * g, 1, [&] { st::launch_reduce(s, g, h->partial, h->dscal); });
     double out = 0;
     ck(cudaMemcpyAsync(&out, h->dscal, sizeof(double), cudaMemcpyDeviceToHost, h->stream), "norm d2h");
     ck(cudaStreamSynchronize(h->stream), "sync");
@@ -294,11 +305,12 @@ int st_setup(const st_params *p, st_handle **out) {
         h->dl.resize(h->hl.size());
         ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
         h->own_stream = true;
+        if (const char *dbg = std::getenv("ST_DEBUG_SYNC")) h->debug_sync = dbg[0] == '1';
         size_t max_partial = 1;
         for (size_t l = 0; l < h->hl.size(); ++l) {
             st::HostLevel &H = h->hl[l];
             DevLevel &D = h->dl[l];
-            D.n_edges = H.mesh.n_edges; D.n_nodes = H.mesh.n_nodes; D.S = (int)H.tau.size();
+            D.n_edges = H.mesh.n_edges; D.n_nodes = H.mesh.n_nodes; D.S = (int)H.tau.size(); D.Q = Q;
             if ((long long)D.n_edges * D.S >= (1LL << 31) || (long long)D.n_nodes * 32 >= (1LL << 31))
                 throw Unsupported("level too large for 32-bit thread indexing");
             D.M = h->upload(H.M); D.K = h->upload(H.K); D.Kn = h->upload(H.Kn); D.GT = h->upload(H.GT);
@@ -309,7 +321,7 @@ int st_setup(const st_params *p, st_handle **out) {
             D.nbox_e = (int)H.bptr_e.size() - 1; D.nbox_n = (int)H.bptr_n.size() - 1;
             D.tau = h->upload(H.tau);
             D.space_coarsened = H.space_coarsened;
-            if (H.uniform && o.kernel_path == 0) {
+            if (H.uniform && o.kernel_path == 0 && Q <= 2) {
                 const double hx = H.hbox[0], hy = H.hbox[1], hz = H.hbox[2];
                 D.use_march = true;
                 D.grid.nx = H.mesh.n[0]; D.grid.ny = H.mesh.n[1]; D.grid.nz = H.mesh.n[2];

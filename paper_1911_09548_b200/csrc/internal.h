@@ -77,7 +77,7 @@ struct Grid3 {
 };
 
 struct DevLevel {
-    int n_edges = 0, n_nodes = 0, S = 0;
+    int n_edges = 0, n_nodes = 0, S = 0, Q = 1;
     DevELL M, K, Kn, GT, Pg, Rg;
     double *dM = nullptr, *dK = nullptr, *dN = nullptr;
     int *edge_nodes = nullptr;

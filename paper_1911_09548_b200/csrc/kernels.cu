@@ -584,16 +584,19 @@ __global__ void __launch_bounds__(kBlock) k_g_update(BoxMap m, const int *__rest
 
 // ------------------------------------------------ pencil march (uniform hex levels)
 // Grid: blocks ordered slab-chunk-major; block = 4 warps = 4 consecutive pencils (j, k)
-// of one slab chunk.  HALO (residual): lane 0 is the slab before the chunk so that its
-// mass image of time node q feeds lane 1's upwind coupling by a shuffle; chunk stride 31.
+// of one slab chunk.  Lane = (slab, time node a) with a fastest (Q = 1 or 2 lanes per
+// slab), so every thread carries the march window of ONE time node; the time-matrix
+// combination exchanges the partner lane's images with shfl_xor.  HALO (residual): the
+// first slab of the warp is the slab before the chunk, whose mass image of time node q
+// feeds the next slab's upwind coupling by a shuffle; chunk stride = 32/Q - 1 slabs.
 struct MarchMap {
     int S, n_pencils, n_pblocks, stride;
 };
 constexpr int kMarchWarps = 4;
 
-template <bool HALO>
-__device__ __forceinline__ void march_coords(const MarchMap &mm, const Grid3 &g, int &j, int &k, int &ks, bool &out_ok,
-                                             bool &pencil_ok) {
+template <int Q, bool HALO>
+__device__ __forceinline__ void march_coords(const MarchMap &mm, const Grid3 &g, int &j, int &k, int &ks, int &a,
+                                             bool &out_ok, bool &pencil_ok) {
     const int chunk = blockIdx.x / mm.n_pblocks;
     const int pb = blockIdx.x - chunk * mm.n_pblocks;
     const int p = pb * kMarchWarps + (threadIdx.x >> 5);
@@ -602,66 +605,100 @@ __device__ __forceinline__ void march_coords(const MarchMap &mm, const Grid3 &g,
     j = pp % (g.ny + 1);
     k = pp / (g.ny + 1);
     const int lane = threadIdx.x & 31;
-    ks = HALO ? chunk * 31 + lane - 1 : chunk * 32 + lane;
-    out_ok = (HALO ? lane >= 1 : true) && ks < mm.S;
+    a = lane % Q;
+    const int sl = lane / Q;
+    ks = chunk * mm.stride + sl - (HALO ? 1 : 0);
+    out_ok = (HALO ? sl >= 1 : true) && ks < mm.S;
     if (ks >= mm.S) ks = mm.S - 1;
 }
 
+// the (Q x Q) time combination for the lane's own test index b = a:
+//   (A x)_b = sum_a' Ct[b][a'] M_a' + t Mt[b][a'] K_a'   with M_a', K_a' of the partner lanes
+template <int Q>
+__device__ __forceinline__ double time_combine(const KT &kt, int b, double t, double mimg, double kimg) {
+    double acc = 0.0;
+#pragma unroll
+    for (int ap = 0; ap < Q; ++ap) {
+        const double mo = Q == 1 ? mimg : __shfl_sync(0xffffffffu, mimg, ((threadIdx.x & 31) & ~(Q - 1)) + ap);
+        const double ko = Q == 1 ? kimg : __shfl_sync(0xffffffffu, kimg, ((threadIdx.x & 31) & ~(Q - 1)) + ap);
+        acc += kt.Ct[b * Q + ap] * mo + t * kt.Mt[b * Q + ap] * ko;
+    }
+    return acc;
+}
+
+// y_b = (D^{-1} v)_b for the lane's own b, D = Ct dm + t Mt dk, v spread over the Q lanes of a slab
+template <int Q>
+__device__ __forceinline__ double block_solve_lanes(const KT &kt, int b, double dm, double dk, double t, double vb) {
+    double v[Q], y[Q];
+#pragma unroll
+    for (int ap = 0; ap < Q; ++ap)
+        v[ap] = Q == 1 ? vb : __shfl_sync(0xffffffffu, vb, ((threadIdx.x & 31) & ~(Q - 1)) + ap);
+    block_solve<Q>(kt, dm, dk, t, v, y);
+    double out = y[0];
+#pragma unroll
+    for (int ap = 1; ap < Q; ++ap)
+        if (b == ap) out = y[ap];
+    return out;
+}
+
+template <int Q>
+__device__ __forceinline__ double block_mul_lanes(const KT &kt, int b, double dm, double dk, double t, double vb) {
+    double v[Q], y[Q];
+#pragma unroll
+    for (int ap = 0; ap < Q; ++ap)
+        v[ap] = Q == 1 ? vb : __shfl_sync(0xffffffffu, vb, ((threadIdx.x & 31) & ~(Q - 1)) + ap);
+    block_mul<Q>(kt, dm, dk, t, v, y);
+    double out = y[0];
+#pragma unroll
+    for (int ap = 1; ap < Q; ++ap)
+        if (b == ap) out = y[ap];
+    return out;
+}
+
 template <int Q, bool R_OUT, bool Z_OUT, bool NORM>
-__global__ void __launch_bounds__(32 * kMarchWarps) k_res_march(MarchMap mm, Grid3 g, const double *__restrict__ tau,
+__global__ void __launch_bounds__(32 * kMarchWarps, 3) k_res_march(MarchMap mm, Grid3 g, const double *__restrict__ tau,
                                                                 const double *__restrict__ x,
                                                                 const double *__restrict__ f,
                                                                 const double *__restrict__ prev, double *__restrict__ r,
                                                                 double *__restrict__ z, const double *__restrict__ dM,
                                                                 const double *__restrict__ dK, double omega_s, KT kt,
                                                                 double *__restrict__ partial) {
-    int j, k, ks;
+    int j, k, ks, a;
     bool out_ok, pencil_ok;
-    march_coords<true>(mm, g, j, k, ks, out_ok, pencil_ok);
+    march_coords<Q, true>(mm, g, j, k, ks, a, out_ok, pencil_ok);
     double nrm = 0.0;
     if (pencil_ok) {
         const int S = mm.S, QS = Q * S;
         const Lane ln{x, prev, S, QS, ks, Q - 1};
         const double t = ks >= 0 ? __ldg(tau + ks) : 0.0;
-        Win w[Q];
-#pragma unroll
-        for (int a = 0; a < Q; ++a) win_init(g, ln, a, j, k, w[a]);
-        Cells c;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) { (&c.s[0][0][0])[u] = 0.0; (&c.n[0][0][0])[u] = 0.0; }
+        Win w;
+        win_init(g, ln, a, j, k, w);
+        StepLoads cur, nxt;
+        load_step(g, ln, a, 0, j, k, cur);
         for (int i = 0; i <= g.nx; ++i) {
-            load_cells(g, i, j, k, c);
-            double o[Q][6];
-#pragma unroll
-            for (int a = 0; a < Q; ++a) step(g, ln, c, a, i, j, k, w[a], o[a]);
+            if (i < g.nx) load_step(g, ln, a, i + 1, j, k, nxt);   // software pipeline: next step's gathers in flight
+            Cells c;
+            load_cells2(g, i, j, k, c);
+            double o[6];
+            step(g, c, cur, w, o);
+            cur = nxt;
 #pragma unroll
             for (int e = 0; e < 3; ++e) {
                 const bool exists = e == 0 ? i < g.nx : (e == 1 ? j < g.ny : k < g.nz);   // warp-uniform
                 if (!exists) continue;
-                const double mp = __shfl_up_sync(0xffffffffu, o[Q - 1][e], 1);
+                // upwind coupling: time node 0 of slab ks takes the mass image of node q of slab ks-1
+                const double mp = __shfl_up_sync(0xffffffffu, o[e], 1);
+                const double ax = time_combine<Q>(kt, a, t, o[e], o[3 + e]);
                 const int row = e == 0 ? xid(g, i, j, k) : (e == 1 ? yid(g, i, j, k) : zid(g, i, j, k));
-                if (!out_ok) continue;
-                const size_t base = (size_t)row * QS + ks;
-                double rr[Q];
-#pragma unroll
-                for (int b = 0; b < Q; ++b) {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int a = 0; a < Q; ++a) acc += kt.Ct[b * Q + a] * o[a][e] + t * kt.Mt[b * Q + a] * o[a][3 + e];
-                    rr[b] = __ldg(f + base + b * S) - acc + (b == 0 ? mp : 0.0);
-                }
-                if (R_OUT)
-#pragma unroll
-                    for (int b = 0; b < Q; ++b) r[base + b * S] = rr[b];
+                const size_t idx = (size_t)row * QS + a * S + ks;
+                // (the halo lane of chunk 0 has ks = -1: never touch f there)
+                const double rr = (out_ok ? __ldg(f + idx) : 0.0) - ax + (a == 0 ? mp : 0.0);
+                if (R_OUT && out_ok) r[idx] = rr;
                 if (Z_OUT) {
-                    double y[Q];
-                    block_solve<Q>(kt, __ldg(dM + row), __ldg(dK + row), t, rr, y);
-#pragma unroll
-                    for (int b = 0; b < Q; ++b) z[base + b * S] = omega_s * y[b];
+                    const double y = block_solve_lanes<Q>(kt, a, __ldg(dM + row), __ldg(dK + row), t, rr);
+                    if (out_ok) z[idx] = omega_s * y;
                 }
-                if (NORM)
-#pragma unroll
-                    for (int b = 0; b < Q; ++b) nrm += rr[b] * rr[b];
+                if (NORM && out_ok) nrm += rr * rr;
             }
         }
     }
@@ -675,64 +712,44 @@ __global__ void __launch_bounds__(32 * kMarchWarps) k_res_march(MarchMap mm, Gri
 // Jacobi sweep on A_k with the march: znew = z + omega_s D^{-1}(r - A_k z), r = D z / omega_s
 // (RECON) or read; LAST: x += omega znew, else out = znew.
 template <int Q, bool LAST, bool RECON>
-__global__ void __launch_bounds__(32 * kMarchWarps) k_sweep_march(MarchMap mm, Grid3 g, const double *__restrict__ tau,
+__global__ void __launch_bounds__(32 * kMarchWarps, 3) k_sweep_march(MarchMap mm, Grid3 g, const double *__restrict__ tau,
                                                                   const double *__restrict__ dM,
                                                                   const double *__restrict__ dK,
                                                                   const double *__restrict__ z,
                                                                   const double *__restrict__ r, double *out,
                                                                   double omega_s, double omega, KT kt) {
-    int j, k, ks;
+    int j, k, ks, a;
     bool out_ok, pencil_ok;
-    march_coords<false>(mm, g, j, k, ks, out_ok, pencil_ok);
+    march_coords<Q, false>(mm, g, j, k, ks, a, out_ok, pencil_ok);
     if (!pencil_ok) return;
     const int S = mm.S, QS = Q * S;
     const Lane ln{z, nullptr, S, QS, ks, Q - 1};
     const double t = __ldg(tau + ks);
-    Win w[Q];
-#pragma unroll
-    for (int a = 0; a < Q; ++a) win_init(g, ln, a, j, k, w[a]);
-    Cells c;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) { (&c.s[0][0][0])[u] = 0.0; (&c.n[0][0][0])[u] = 0.0; }
+    Win w;
+    win_init(g, ln, a, j, k, w);
+    StepLoads cur, nxt;
+    load_step(g, ln, a, 0, j, k, cur);
     for (int i = 0; i <= g.nx; ++i) {
-        load_cells(g, i, j, k, c);
-        double o[Q][6];
-#pragma unroll
-        for (int a = 0; a < Q; ++a) step(g, ln, c, a, i, j, k, w[a], o[a]);
-        if (!out_ok) continue;
+        if (i < g.nx) load_step(g, ln, a, i + 1, j, k, nxt);
+        Cells c;
+        load_cells2(g, i, j, k, c);
+        double o[6];
+        step(g, c, cur, w, o);
+        cur = nxt;
 #pragma unroll
         for (int e = 0; e < 3; ++e) {
             const bool exists = e == 0 ? i < g.nx : (e == 1 ? j < g.ny : k < g.nz);
             if (!exists) continue;
             const int row = e == 0 ? xid(g, i, j, k) : (e == 1 ? yid(g, i, j, k) : zid(g, i, j, k));
-            const size_t base = (size_t)row * QS + ks;
+            const size_t idx = (size_t)row * QS + a * S + ks;
             const double dm = __ldg(dM + row), dk = __ldg(dK + row);
-            double zr[Q], rv[Q], d[Q], y[Q];
-#pragma unroll
-            for (int a = 0; a < Q; ++a) zr[a] = z[base + a * S];
-            if (RECON) {
-                block_mul<Q>(kt, dm, dk, t, zr, rv);
-#pragma unroll
-                for (int a = 0; a < Q; ++a) rv[a] /= omega_s;
-            } else {
-#pragma unroll
-                for (int a = 0; a < Q; ++a) rv[a] = __ldg(r + base + a * S);
-            }
-#pragma unroll
-            for (int b = 0; b < Q; ++b) {
-                double acc = 0.0;
-#pragma unroll
-                for (int a = 0; a < Q; ++a) acc += kt.Ct[b * Q + a] * o[a][e] + t * kt.Mt[b * Q + a] * o[a][3 + e];
-                d[b] = rv[b] - acc;
-            }
-            block_solve<Q>(kt, dm, dk, t, d, y);
-            if (LAST) {
-#pragma unroll
-                for (int a = 0; a < Q; ++a) out[base + a * S] += omega * (zr[a] + omega_s * y[a]);
-            } else {
-#pragma unroll
-                for (int a = 0; a < Q; ++a) out[base + a * S] = zr[a] + omega_s * y[a];
-            }
+            const double zr = z[idx];
+            const double rv = RECON ? block_mul_lanes<Q>(kt, a, dm, dk, t, zr) / omega_s : __ldg(r + idx);
+            const double d = rv - time_combine<Q>(kt, a, t, o[e], o[3 + e]);
+            const double y = block_solve_lanes<Q>(kt, a, dm, dk, t, d);
+            if (!out_ok) continue;
+            if (LAST) out[idx] += omega * (zr + omega_s * y);
+            else out[idx] = zr + omega_s * y;
         }
     }
 }
@@ -913,6 +930,12 @@ static inline BoxMap node_map(const DevLevel &L) { return make_boxmap(L.S, L.sch
         case 3: { constexpr int QQ = 3; __VA_ARGS__; } break;   \
         default: throw std::invalid_argument("Q out of range"); \
     }
+#define ST_DISPATCH_Q12(Q, ...)                                 \
+    switch (Q) {                                                \
+        case 1: { constexpr int QQ = 1; __VA_ARGS__; } break;   \
+        case 2: { constexpr int QQ = 2; __VA_ARGS__; } break;   \
+        default: throw std::invalid_argument("march: Q <= 2");  \
+    }
 #define ST_DISPATCH_SPL(spl, ...)                               \
     if (spl == 2) { constexpr int SP = 2; __VA_ARGS__; }        \
     else { constexpr int SP = 1; __VA_ARGS__; }
@@ -930,18 +953,18 @@ static MarchMap march_map(const DevLevel &L, bool halo) {
     mm.S = L.S;
     mm.n_pencils = (L.grid.ny + 1) * (L.grid.nz + 1);
     mm.n_pblocks = (mm.n_pencils + kMarchWarps - 1) / kMarchWarps;
-    mm.stride = halo ? 31 : 32;
+    mm.stride = 32 / L.Q - (halo ? 1 : 0);
     return mm;
 }
 static inline int grid(const MarchMap &mm) { return mm.n_pblocks * ((mm.S + mm.stride - 1) / mm.stride); }
 
 int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
                     const double *prev, double *r, double *z, double omega_s, double *partial) {
-    if (L.use_march) {
+    if (L.use_march && Q <= 2) {
         const MarchMap mm = march_map(L, true);
         const int g = grid(mm);
         const int nt = 32 * kMarchWarps;
-        ST_DISPATCH_Q(Q, {
+        ST_DISPATCH_Q12(Q, {
             if (partial) {
                 if (r) k_res_march<QQ, true, false, true><<<g, nt, 0, st>>>(mm, L.grid, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
                 else k_res_march<QQ, false, false, true><<<g, nt, 0, st>>>(mm, L.grid, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
@@ -973,15 +996,15 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
 }
 
 int residual_partials(const DevLevel &L) {
-    return L.use_march ? grid(march_map(L, true)) : grid(edge_map(L));
+    return (L.use_march && L.Q <= 2) ? grid(march_map(L, true)) : grid(edge_map(L));
 }
 
 void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, bool recon, const double *z,
                   const double *r, double *out, double omega_s, double omega) {
-    if (L.use_march) {
+    if (L.use_march && Q <= 2) {
         const MarchMap mm = march_map(L, false);
         const int g = grid(mm), nt = 32 * kMarchWarps;
-        ST_DISPATCH_Q(Q, {
+        ST_DISPATCH_Q12(Q, {
             if (last && recon) k_sweep_march<QQ, true, true><<<g, nt, 0, st>>>(mm, L.grid, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
             else if (last) k_sweep_march<QQ, true, false><<<g, nt, 0, st>>>(mm, L.grid, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
             else if (recon) k_sweep_march<QQ, false, true><<<g, nt, 0, st>>>(mm, L.grid, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
