@@ -1,0 +1,82 @@
+"""GPU checks at the BASELINE.json full sizes, in the launch configuration bench.py times.
+
+The oracle cannot run a whole V-cycle there, so (a) the finest-level residual r = f - L x is
+compared on sampled rows that the oracle computes one by one from its own assembled operators,
+and (b) V-cycle properties that hold at any size are checked (contraction, zero-rhs fixed point)."""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import fem, mesh, time_dg
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1911_09548_b200 import build
+    build.build()
+    return torch
+
+
+def sampled_residual(w, X_rows, F_rows, rows, M, K):
+    """Oracle residual at `rows` for all slabs: r = f - sum_a (Ct M + tau Mt K) x_a + Nt M x_{k-1}.
+    X_rows: dict col -> (Q, S) values of every column the sampled rows touch."""
+    Ct, Mt, Nt = time_dg.time_matrices(w.q)
+    out = []
+    for r in rows:
+        mx = sum(M[r, c] * X_rows[c] for c in M[r].indices)
+        kx = sum(K[r, c] * X_rows[c] for c in K[r].indices)
+        R = F_rows[r] - (Ct @ mx) - (Mt @ kx) * w.tau[None, :]
+        R[0, 1:] += mx[w.q, :-1]      # Nt = e_0 e_q^T: time node 0 sees the previous slab's end value
+        out.append(R)
+    return np.array(out)
+
+
+@pytest.mark.parametrize("name", ["c4", "c3", "c5"])
+def test_fullsize_residual_sampled(torch_cuda, name):
+    torch = torch_cuda
+    import paper_1911_09548_b200 as p
+    w = {"c4": lambda: workloads.c4(), "c3": lambda: workloads.c3(), "c5": lambda: workloads.c5()}[name]()
+    s = p.Solver.from_workload(w)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    x = torch.empty(s.shape, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g)
+    f = w.rhs_device()
+    r = torch.empty_like(f)
+    s.residual(x, f, r)
+    m = mesh.Mesh(w.n, w.node_coords())
+    M, K, _ = fem.assemble(m, w.sigma, w.nu)
+    M, K = M.tocsr(), K.tocsr()
+    rng = np.random.default_rng(0)
+    rows = sorted(set(rng.integers(0, m.n_edges, 24).tolist()) | {0, m.n_edges - 1, m.Ex, m.Ex + m.Ey})
+    cols = sorted(set(np.concatenate([K[rr].indices for rr in rows] + [M[rr].indices for rr in rows]).tolist()))
+    idx = torch.tensor(cols, device="cuda")
+    Xc = x.index_select(0, idx).cpu().numpy()
+    X_rows = {c: Xc[i] for i, c in enumerate(cols)}
+    ridx = torch.tensor(rows, device="cuda")
+    F_rows = dict(zip(rows, f.index_select(0, ridx).cpu().numpy()))
+    R_or = sampled_residual(w, X_rows, F_rows, rows, M, K)
+    R_gpu = r.index_select(0, ridx).cpu().numpy()
+    scale = np.abs(R_or).max()
+    assert np.abs(R_gpu - R_or).max() <= 1e-12 * scale, np.abs(R_gpu - R_or).max() / scale
+
+
+@pytest.mark.parametrize("name", ["c4", "c2_lam1", "c1"])
+def test_fullsize_vcycle_contracts(torch_cuda, name):
+    # one V-cycle from zero reduces the relative residual well below 1, and V(0, 0) = 0
+    torch = torch_cuda
+    import paper_1911_09548_b200 as p
+    w = {"c4": lambda: workloads.c4(), "c2_lam1": lambda: workloads.c2(1.0), "c1": lambda: workloads.c1()}[name]()
+    s = p.Solver.from_workload(w)
+    f = w.rhs_device()
+    x = torch.zeros_like(f)
+    it, hist = s.solve(x, f, tol=0.0, maxit=2)
+    assert hist[0] == pytest.approx(1.0)
+    assert hist[1] < 0.5 and hist[2] < 0.5 * hist[1], hist
+    z = torch.zeros_like(f)
+    x0 = torch.zeros_like(f)
+    s.vcycle(x0, z)
+    assert torch.count_nonzero(x0).item() == 0
