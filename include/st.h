@@ -72,6 +72,10 @@ typedef struct st_params {
     int min_slabs;         /* stop time coarsening at this many slabs, default 1 */
     int kernel_path;       /* 0: matrix-free pencil march on uniform hex levels, ELL elsewhere
                               (default); 1: assembled ELL operators everywhere */
+    int rank, nranks;      /* multi-GPU (one process per GPU): nranks <= 1 means single GPU.
+                              With nranks > 1, tau is the GLOBAL slab array; this rank owns the
+                              contiguous block [rank*n_slabs/nranks, (rank+1)*n_slabs/nranks)
+                              and its vectors hold only that block (ST layout with S = block). */
 } st_params;
 
 typedef struct st_info_t {
@@ -130,6 +134,42 @@ typedef struct st_kstat {
 /* Synchronises the stream and returns up to `max` per-family aggregates of
  * the launches recorded since st_profile(h, 1); *n = number of families. */
 int st_profile_read(st_handle *h, st_kstat *out, int max, int *n);
+
+/* ---- level operations: a driver (multi-GPU: paper_1911_09548_b200/distributed.py)
+ * sequences the V-cycle itself around its collectives.  set = 0: this rank's distributed
+ * levels 0..g0 over its slab block; set = 1 (rank 0 of a multi-rank handle only): the
+ * gathered global levels g0..L-1 (index 0 of set 1 is global level g0).  All vector
+ * arguments are device pointers in ST layout for that level's slab count; `prev` is the
+ * time-node-q trace of the slab before the block (n_edges values) or NULL (zero initial
+ * state); `tot` / `carry` hold one value per node (the integrated end value of the nodal
+ * correction's time scan, R2).  Asynchronous unless stated. */
+typedef struct st_level_t {
+    int set, level, global_level;
+    int n_slabs, slab0;          /* slab count of this level in this set, first global slab */
+    int n_edges, n_nodes, q;
+    int coarsest, space_coarsened;
+    double *x, *f;               /* the level's own work vectors (NULL for set 0, level 0) */
+    double *r;                   /* the level's residual scratch (overwritten by every level op) */
+} st_level_t;
+
+int st_lv_count(const st_handle *h, int set, int *n);
+int st_lv_get(const st_handle *h, int set, int level, st_level_t *out);
+/* r = f - L x (r may be NULL); norm2 (host, may be NULL) receives ||r||^2 (synchronises) */
+int st_lv_residual(st_handle *h, int set, int level, const double *x, const double *f, const double *prev,
+                   double *r, double *norm2);
+int st_lv_smooth_S(st_handle *h, int set, int level, double *x, const double *f, const double *prev);  /* Eq. (2) */
+int st_lv_correct_local(st_handle *h, int set, int level, double *x, const double *f, const double *prev,
+                        double *tot);                                                          /* Eq. (5), 1st half */
+int st_lv_correct_apply(st_handle *h, int set, int level, double *x, const double *carry);     /* Eq. (5), 2nd half */
+int st_lv_restrict(st_handle *h, int set, int level, const double *r, double *fc);             /* level -> level+1 */
+int st_lv_prolong(st_handle *h, int set, int level, const double *xc, double *x);              /* x += P xc */
+int st_lv_vcycle(st_handle *h, int set, int level, double *x, const double *f);                /* within the set */
+int st_lv_end_values(st_handle *h, int set, int level, const double *x, double *out);
+/* dst[row][a][dk0+s] (+)= src[row][a][sk0+s] for s < ns, rows x (q+1) rows of slabs */
+int st_copy_slabs(st_handle *h, int rows, int q, int ns, double *dst, int dS, int dk0, const double *src, int sS,
+                  int sk0, int add);
+int st_zero(st_handle *h, double *ptr, int64_t n);
+int st_sync(st_handle *h);
 
 /* Host-only (no CUDA device needed): build the level hierarchy of p on the
  * host and report it in *info (kernel_launches = device_bytes = 0). */

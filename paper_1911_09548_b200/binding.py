@@ -14,9 +14,12 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libst.so")
 
+LEVEL_OPS = ["st_lv_count", "st_lv_get", "st_lv_residual", "st_lv_smooth_S", "st_lv_correct_local",
+             "st_lv_correct_apply", "st_lv_restrict", "st_lv_prolong", "st_lv_vcycle", "st_lv_end_values",
+             "st_copy_slabs", "st_zero", "st_sync"]
 EXPORTED = ["st_setup", "st_free", "st_set_stream", "st_residual", "st_vcycle", "st_solve",
             "st_solve_host", "st_info", "st_profile", "st_profile_read", "st_plan", "st_host_matrix",
-            "st_last_error"]
+            *LEVEL_OPS, "st_last_error"]
 
 
 class StParams(ctypes.Structure):
@@ -27,7 +30,7 @@ class StParams(ctypes.Structure):
                 ("spec", ctypes.c_char_p), ("omega", ctypes.c_double), ("nu_s", ctypes.c_int),
                 ("omega_s", ctypes.c_double), ("nu_n", ctypes.c_int), ("omega_n", ctypes.c_double),
                 ("lambda_crit", ctypes.c_double), ("mode", ctypes.c_int), ("min_slabs", ctypes.c_int),
-                ("kernel_path", ctypes.c_int)]
+                ("kernel_path", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int)]
 
 
 class StInfo(ctypes.Structure):
@@ -36,6 +39,14 @@ class StInfo(ctypes.Structure):
                 ("level_n_slabs", ctypes.c_int * 32), ("level_space_coarsened", ctypes.c_int * 32),
                 ("level_lambda", ctypes.c_double * 32), ("kernel_launches", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("level_matrix_free", ctypes.c_int * 32)]
+
+
+class StLevel(ctypes.Structure):
+    _fields_ = [("set", ctypes.c_int), ("level", ctypes.c_int), ("global_level", ctypes.c_int),
+                ("n_slabs", ctypes.c_int), ("slab0", ctypes.c_int), ("n_edges", ctypes.c_int),
+                ("n_nodes", ctypes.c_int), ("q", ctypes.c_int), ("coarsest", ctypes.c_int),
+                ("space_coarsened", ctypes.c_int), ("x", ctypes.c_void_p), ("f", ctypes.c_void_p),
+                ("r", ctypes.c_void_p)]
 
 
 class StKstat(ctypes.Structure):
@@ -67,6 +78,21 @@ def load():
     lib.st_profile_read.argtypes = [vp, ctypes.POINTER(StKstat), ctypes.c_int, ip]
     lib.st_plan.argtypes = [ctypes.POINTER(StParams), ctypes.POINTER(StInfo)]
     lib.st_host_matrix.argtypes = [ctypes.POINTER(StParams), ctypes.c_int, ctypes.c_int, ip, ip, ip, dp]
+    i64 = ctypes.c_int64
+    ci = ctypes.c_int
+    lib.st_lv_count.argtypes = [vp, ci, ip]
+    lib.st_lv_get.argtypes = [vp, ci, ci, ctypes.POINTER(StLevel)]
+    lib.st_lv_residual.argtypes = [vp, ci, ci, vp, vp, vp, vp, dp]
+    lib.st_lv_smooth_S.argtypes = [vp, ci, ci, vp, vp, vp]
+    lib.st_lv_correct_local.argtypes = [vp, ci, ci, vp, vp, vp, vp]
+    lib.st_lv_correct_apply.argtypes = [vp, ci, ci, vp, vp]
+    lib.st_lv_restrict.argtypes = [vp, ci, ci, vp, vp]
+    lib.st_lv_prolong.argtypes = [vp, ci, ci, vp, vp]
+    lib.st_lv_vcycle.argtypes = [vp, ci, ci, vp, vp]
+    lib.st_lv_end_values.argtypes = [vp, ci, ci, vp, vp]
+    lib.st_copy_slabs.argtypes = [vp, ci, ci, ci, vp, ci, ci, vp, ci, ci, ci]
+    lib.st_zero.argtypes = [vp, vp, i64]
+    lib.st_sync.argtypes = [vp]
     lib.st_last_error.restype = ctypes.c_char_p
     for name in EXPORTED[:-1]:
         getattr(lib, name).restype = ctypes.c_int
@@ -88,7 +114,7 @@ def _dptr(a):
 
 
 def make_params(dim, n, sigma, nu, tau, q=1, coords=None, spec="SAS", omega=0.5, nu_s=2, omega_s=None,
-                nu_n=2, omega_n=0.6, lambda_crit=0.1, mode=0, min_slabs=1, kernel_path=0):
+                nu_n=2, omega_n=0.6, lambda_crit=0.1, mode=0, min_slabs=1, kernel_path=0, rank=0, nranks=1):
     """Fill an StParams; returns (params, keep-alive list)."""
     keep = [np.ascontiguousarray(sigma, dtype=np.float64), np.ascontiguousarray(nu, dtype=np.float64),
             np.ascontiguousarray(tau, dtype=np.float64), spec.encode()]
@@ -108,6 +134,7 @@ def make_params(dim, n, sigma, nu, tau, q=1, coords=None, spec="SAS", omega=0.5,
     p.omega_s = omega_s if omega_s is not None else (0.6 if dim == 3 else 0.5)
     p.lambda_crit, p.mode, p.min_slabs = lambda_crit, mode, min_slabs
     p.kernel_path = kernel_path
+    p.rank, p.nranks = rank, nranks
     return p, keep
 
 
@@ -147,15 +174,18 @@ class Solver:
     """Handle over st_setup for one workload (see workloads.Workload for the fields)."""
 
     def __init__(self, dim, n, sigma, nu, tau, q=1, coords=None, spec="SAS", omega=0.5, nu_s=2, omega_s=None,
-                 nu_n=2, omega_n=0.6, lambda_crit=0.1, mode=0, min_slabs=1, kernel_path=0, stream=None):
+                 nu_n=2, omega_n=0.6, lambda_crit=0.1, mode=0, min_slabs=1, kernel_path=0, rank=0, nranks=1,
+                 stream=None):
         import torch
         if not torch.cuda.is_available():
             raise StError("no CUDA device: the space-time multigrid has no CPU path")
         lib = load()
         p, self._keep = make_params(dim, n, sigma, nu, tau, q=q, coords=coords, spec=spec, omega=omega, nu_s=nu_s,
                                     omega_s=omega_s, nu_n=nu_n, omega_n=omega_n, lambda_crit=lambda_crit, mode=mode,
-                                    min_slabs=min_slabs, kernel_path=kernel_path)
-        self.dim, self.n, self.q, self.S = dim, tuple(n), q, p.n_slabs
+                                    min_slabs=min_slabs, kernel_path=kernel_path, rank=rank, nranks=nranks)
+        self.dim, self.n, self.q = dim, tuple(n), q
+        self.rank, self.nranks = rank, max(nranks, 1)
+        self.S = p.n_slabs // self.nranks          # slabs of this rank's block
         h = ctypes.c_void_p()
         _check(lib.st_setup(ctypes.byref(p), ctypes.byref(h)))
         self._h = h
@@ -215,6 +245,47 @@ class Solver:
         hist = (ctypes.c_double * (maxit + 1))()
         _check(load().st_solve_host(self._h, _dptr(x), _dptr(f), tol, maxit, ctypes.byref(it), hist))
         return it.value, list(hist[: it.value + 1])
+
+    # ---- level operations (multi-GPU driver: distributed.py) -------------------------
+    def level(self, set_, level):
+        out = StLevel()
+        _check(load().st_lv_get(self._h, set_, level, ctypes.byref(out)))
+        return out
+
+    def n_levels(self, set_):
+        n = ctypes.c_int()
+        _check(load().st_lv_count(self._h, set_, ctypes.byref(n)))
+        return n.value
+
+    def lv(self, name, *args):
+        """Call st_lv_<name>(handle, *args); tensors are passed as device pointers, None as NULL."""
+        conv = []
+        for a in args:
+            if a is None:
+                conv.append(None)
+            elif hasattr(a, "data_ptr"):
+                conv.append(ctypes.c_void_p(a.data_ptr()))
+            else:
+                conv.append(a)
+        _check(getattr(load(), "st_lv_" + name)(self._h, *conv))
+
+    def lv_residual_norm2(self, set_, level, x, f, prev):
+        out = ctypes.c_double()
+        _check(load().st_lv_residual(self._h, set_, level, ctypes.c_void_p(x.data_ptr()),
+                                     ctypes.c_void_p(f.data_ptr()),
+                                     ctypes.c_void_p(prev.data_ptr()) if prev is not None else None,
+                                     None, ctypes.byref(out)))
+        return out.value
+
+    def copy_slabs(self, rows, ns, dst, dS, dk0, src, sS, sk0, add=False):
+        _check(load().st_copy_slabs(self._h, rows, self.q, ns, ctypes.c_void_p(dst.data_ptr()), dS, dk0,
+                                    ctypes.c_void_p(src.data_ptr()), sS, sk0, 1 if add else 0))
+
+    def zero(self, t):
+        _check(load().st_zero(self._h, ctypes.c_void_p(t.data_ptr()), t.numel()))
+
+    def sync(self):
+        _check(load().st_sync(self._h))
 
     def profile(self, enable=True):
         _check(load().st_profile(self._h, 1 if enable else 0))

@@ -39,7 +39,9 @@ struct st_handle {
     st::KT kt{};
     int Q = 1;
     std::vector<st::HostLevel> hl;
-    std::vector<st::DevLevel> dl;
+    std::vector<st::DevLevel> dl;   // this rank's levels 0..(g0 or L-1), local slab blocks
+    std::vector<st::DevLevel> dg;   // rank 0 of a multi-rank run: global levels g0..L-1 ("gathered")
+    int rank = 0, nranks = 1, g0 = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     double *partial = nullptr;
@@ -139,18 +141,20 @@ double op_bytes(const DevLevel &L) { return ell_bytes(L.M) + ell_bytes(L.K) + 16
 double evec(const DevLevel &L, int Q) { return 8.0 * L.n_edges * Q * L.S; }
 double nvec(const DevLevel &L, int Q) { return 8.0 * L.n_nodes * Q * L.S; }
 
-void smooth_S(st_handle *h, DevLevel &L, double *x, const double *f) {
+// prev: end values (time node q) of the slab before this level's first slab (the previous
+// rank's last slab), or null for the zero initial state (PAPER.md l.47-48 homogeneous u^0)
+void smooth_S(st_handle *h, DevLevel &L, double *x, const double *f, const double *prev) {
     const auto &o = h->o;
     auto s = (st::Stream)h->stream;
     const int Q = h->Q;
     const double ev = evec(L, Q), ob = op_bytes(L);
     if (o.nu_s == 1) {
-        h->run("residual", 3 * ev + ob, 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, nullptr, nullptr, L.z, o.omega_s, nullptr); });
+        h->run("residual", 3 * ev + ob, 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, prev, nullptr, L.z, o.omega_s, nullptr); });
         h->run("axpy", 3 * ev, 1, [&] { st::launch_axpy(s, vec_len(L, Q), o.omega, L.z, x); });
         return;
     }
     h->run("residual", (o.nu_s > 2 ? 4 : 3) * ev + ob, 1, [&] {
-        st::launch_residual(s, L, h->kt, Q, x, f, nullptr, o.nu_s > 2 ? L.r : nullptr, L.z, o.omega_s, nullptr);
+        st::launch_residual(s, L, h->kt, Q, x, f, prev, o.nu_s > 2 ? L.r : nullptr, L.z, o.omega_s, nullptr);
     });
     double *cur = L.z, *other = L.z2;
     for (int i = 2; i < o.nu_s; ++i) {
@@ -162,12 +166,14 @@ void smooth_S(st_handle *h, DevLevel &L, double *x, const double *f) {
     });
 }
 
-void correct_A(st_handle *h, DevLevel &L, double *x, const double *f) {
+// first half of the nodal correction: r, G^T r, nodal sweeps and the local time scan into L.y;
+// tot (optional, n_nodes) receives each node's integrated end value (rank carry)
+void correct_A_local(st_handle *h, DevLevel &L, double *x, const double *f, const double *prev, double *tot) {
     const auto &o = h->o;
     auto s = (st::Stream)h->stream;
     const int Q = h->Q;
     const double ev = evec(L, Q), nv = nvec(L, Q), kb = ell_bytes(L.Kn) + 8.0 * L.n_nodes;
-    h->run("residual", 3 * ev + op_bytes(L), 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, nullptr, L.r, nullptr, o.omega_s, nullptr); });
+    h->run("residual", 3 * ev + op_bytes(L), 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, prev, L.r, nullptr, o.omega_s, nullptr); });
     h->run("gt", ev + (o.nu_n > 2 ? 2 : 1) * nv + 8.0 * L.n_nodes, 1, [&] { st::launch_gt(s, L, Q, L.r, o.omega_n, L.zn, o.nu_n > 2 ? L.wn : nullptr); });
     double *cur = L.zn, *other = L.zn2;
     int mode = o.nu_n == 1 ? 0 : (o.nu_n == 2 ? 1 : 2);
@@ -175,37 +181,61 @@ void correct_A(st_handle *h, DevLevel &L, double *x, const double *f) {
         h->run("node_sweep", 3 * nv + kb, 1, [&] { st::launch_node_sweep(s, L, Q, cur, L.wn, o.omega_n, other); });
         std::swap(cur, other);
     }
-    h->run("node_scan", (mode == 2 ? 3 : 2) * nv + kb, 1, [&] { st::launch_node_scan(s, L, h->kt, Q, mode, cur, L.wn, o.omega_n, nullptr, L.y, nullptr); });
-    h->run("g_update", 2 * ev + nv + 8.0 * L.n_edges, 1, [&] { st::launch_g_update(s, L, Q, L.y, x); });
+    h->run("node_scan", (mode == 2 ? 3 : 2) * nv + kb, 1, [&] { st::launch_node_scan(s, L, h->kt, Q, mode, cur, L.wn, o.omega_n, nullptr, L.y, tot); });
+}
+
+// second half: x += G (y + g carry), carry (optional, n_nodes) = end value before this block
+void correct_A_apply(st_handle *h, DevLevel &L, double *x, const double *carry) {
+    auto s = (st::Stream)h->stream;
+    const int Q = h->Q;
+    h->run("g_update", 2 * evec(L, Q) + nvec(L, Q) + 8.0 * L.n_edges, 1, [&] { st::launch_g_update(s, L, h->kt, Q, L.y, carry, x); });
+}
+
+void correct_A(st_handle *h, DevLevel &L, double *x, const double *f, const double *prev) {
+    correct_A_local(h, L, x, f, prev, nullptr);
+    correct_A_apply(h, L, x, nullptr);
 }
 
 void hybrid(st_handle *h, DevLevel &L, double *x, const double *f, bool pre) {
     std::string seq = h->o.spec;
     if (!pre) std::reverse(seq.begin(), seq.end());
     for (int i = (int)seq.size() - 1; i >= 0; --i) {   // right to left (l.208)
-        if (seq[i] == 'S') smooth_S(h, L, x, f);
-        else correct_A(h, L, x, f);
+        if (seq[i] == 'S') smooth_S(h, L, x, f, nullptr);
+        else correct_A(h, L, x, f, nullptr);
     }
 }
 
-void vcycle(st_handle *h, int l, double *x, const double *f) {
-    DevLevel &L = h->dl[l];
+void restrict_to(st_handle *h, DevLevel &L, DevLevel &C, const double *r, double *fc) {
     auto s = (st::Stream)h->stream;
     const int Q = h->Q;
-    if (l == (int)h->dl.size() - 1) {
+    h->run("restrict", evec(L, Q) + evec(C, Q) + (L.space_coarsened ? ell_bytes(L.Rg) : 0.0), 1,
+           [&] { st::launch_restrict(s, L, C, Q, r, fc); });
+}
+
+void prolong_from(st_handle *h, DevLevel &L, DevLevel &C, const double *xc, double *x) {
+    auto s = (st::Stream)h->stream;
+    const int Q = h->Q;
+    h->run("prolong", 2 * evec(L, Q) + evec(C, Q) + (L.space_coarsened ? ell_bytes(L.Pg) : 0.0), 1,
+           [&] { st::launch_prolong(s, L, Q, xc, x); });
+}
+
+// single-process V-cycle over the level vector V from level l (the last entry is the coarsest)
+void vcycle(st_handle *h, std::vector<DevLevel> &V, int l, double *x, const double *f) {
+    DevLevel &L = V[l];
+    auto s = (st::Stream)h->stream;
+    const int Q = h->Q;
+    if (l == (int)V.size() - 1) {
         const double N = (double)Q * L.n_edges;
         h->run("coarsest", L.S * (N * N * 8.0 + 2 * evec(L, Q) / L.S), L.S, [&] { st::launch_coarsest(s, L, Q, f, x); });
         return;
     }
     hybrid(h, L, x, f, true);
-    DevLevel &C = h->dl[l + 1];
+    DevLevel &C = V[l + 1];
     h->run("residual", 3 * evec(L, Q) + op_bytes(L), 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, nullptr, L.r, nullptr, h->o.omega_s, nullptr); });
-    h->run("restrict", evec(L, Q) + evec(C, Q) + (L.space_coarsened ? ell_bytes(L.Rg) : 0.0), 1,
-           [&] { st::launch_restrict(s, L, C, Q, L.r, C.f); });
-    if (l + 1 < (int)h->dl.size() - 1) ck(cudaMemsetAsync(C.x, 0, sizeof(double) * vec_len(C, Q), h->stream), "memset");
-    vcycle(h, l + 1, C.x, C.f);
-    h->run("prolong", 2 * evec(L, Q) + evec(C, Q) + (L.space_coarsened ? ell_bytes(L.Pg) : 0.0), 1,
-           [&] { st::launch_prolong(s, L, Q, C.x, x); });
+    restrict_to(h, L, C, L.r, C.f);
+    if (l + 1 < (int)V.size() - 1) ck(cudaMemsetAsync(C.x, 0, sizeof(double) * vec_len(C, Q), h->stream), "memset");
+    vcycle(h, V, l + 1, C.x, C.f);
+    prolong_from(h, L, C, C.x, x);
     hybrid(h, L, x, f, false);
 }
 
@@ -285,6 +315,8 @@ static void parse_options(const st_params *p, st::Options &o) {
     o.mode = p->mode;
     if (p->min_slabs > 0) o.min_slabs = p->min_slabs;
     if (p->kernel_path < 0 || p->kernel_path > 1) throw std::invalid_argument("kernel_path must be 0 or 1");
+    if (p->nranks > 1 && (p->rank < 0 || p->rank >= p->nranks)) throw std::invalid_argument("rank out of range");
+    if (p->nranks > 1 && p->n_slabs % p->nranks) throw std::invalid_argument("n_slabs must be a multiple of nranks");
     o.kernel_path = p->kernel_path;
 }
 
@@ -302,15 +334,23 @@ int st_setup(const st_params *p, st_handle **out) {
         h->Q = h->tm.Q;
         st::build_hierarchy(*p, o, h->tm, h->hl);
         const int Q = h->Q;
-        h->dl.resize(h->hl.size());
+        h->rank = p->nranks > 1 ? p->rank : 0;
+        h->nranks = p->nranks > 1 ? p->nranks : 1;
+        const int P = h->nranks, L = (int)h->hl.size();
+        // distributed levels: S_l divisible by P with at least one slab per rank; the last of
+        // them (g0) is where the V-cycle hands over to the gathered global levels (rank 0)
+        int nd = 0;
+        while (nd < L && (int)h->hl[nd].tau.size() >= P && (int)h->hl[nd].tau.size() % P == 0) ++nd;
+        if (nd == 0) throw std::invalid_argument("n_slabs must be a multiple of nranks");
+        h->g0 = P > 1 ? nd - 1 : L - 1;
         ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
         h->own_stream = true;
         if (const char *dbg = std::getenv("ST_DEBUG_SYNC")) h->debug_sync = dbg[0] == '1';
         size_t max_partial = 1;
-        for (size_t l = 0; l < h->hl.size(); ++l) {
+        auto build = [&](int l, int b, int cnt, bool coarsest, bool alloc_x) {
             st::HostLevel &H = h->hl[l];
-            DevLevel &D = h->dl[l];
-            D.n_edges = H.mesh.n_edges; D.n_nodes = H.mesh.n_nodes; D.S = (int)H.tau.size(); D.Q = Q;
+            DevLevel D;
+            D.n_edges = H.mesh.n_edges; D.n_nodes = H.mesh.n_nodes; D.S = cnt; D.Q = Q;
             if ((long long)D.n_edges * D.S >= (1LL << 31) || (long long)D.n_nodes * 32 >= (1LL << 31))
                 throw Unsupported("level too large for 32-bit thread indexing");
             D.M = h->upload(H.M); D.K = h->upload(H.K); D.Kn = h->upload(H.Kn); D.GT = h->upload(H.GT);
@@ -319,7 +359,7 @@ int st_setup(const st_params *p, st_handle **out) {
             D.sched_e = h->upload(H.sched_e); D.bptr_e = h->upload(H.bptr_e);
             D.sched_n = h->upload(H.sched_n); D.bptr_n = h->upload(H.bptr_n);
             D.nbox_e = (int)H.bptr_e.size() - 1; D.nbox_n = (int)H.bptr_n.size() - 1;
-            D.tau = h->upload(H.tau);
+            D.tau = h->upload(std::vector<double>(H.tau.begin() + b, H.tau.begin() + b + cnt));
             D.space_coarsened = H.space_coarsened;
             if (H.uniform && o.kernel_path == 0 && Q <= 2) {
                 const double hx = H.hbox[0], hy = H.hbox[1], hz = H.hbox[2];
@@ -331,27 +371,35 @@ int st_setup(const st_params *p, st_handle **out) {
                 D.grid.sigma = h->upload(H.sigma);
                 D.grid.nu = h->upload(H.nu);
             }
-            const bool coarsest = l + 1 == h->hl.size();
-            if (!coarsest) {
-                D.Pt = h->upload(H.Pt);
-                if (H.space_coarsened) { D.Pg = h->upload(H.Pg); D.Rg = h->upload(H.Rg); }
-            } else {
-                D.Ainv = h->upload(H.Ainv);
+            if (!coarsest && l + 1 < L && cnt % 2 == 0) {
+                const size_t per = (size_t)2 * Q * Q;
+                D.Pt = h->upload(std::vector<double>(H.Pt.begin() + (b / 2) * per, H.Pt.begin() + ((b + cnt) / 2) * per));
+            }
+            if (!coarsest && l + 1 < L && H.space_coarsened) { D.Pg = h->upload(H.Pg); D.Rg = h->upload(H.Rg); }
+            if (coarsest) {
+                D.Ainv = h->upload(std::vector<double>(H.Ainv.begin() + (size_t)b * Q * D.n_edges * Q * D.n_edges,
+                                                       H.Ainv.begin() + (size_t)(b + cnt) * Q * D.n_edges * Q * D.n_edges));
                 if ((size_t)Q * D.n_edges * sizeof(double) > 48 * 1024) throw Unsupported("coarsest level too large");
             }
             const size_t ve = vec_len(D, Q), vn = vec_len(D, Q, true);
-            if (l > 0) { D.x = h->dalloc<double>(ve); D.f = h->dalloc<double>(ve); }
-            if (!coarsest) {
-                D.r = h->dalloc<double>(ve);
-                D.z = o.nu_s > 2 ? h->dalloc<double>(ve) : D.r;   // r and z are never live together for nu_s <= 2
-                if (o.nu_s > 2) D.z2 = h->dalloc<double>(ve);
-                D.zn = h->dalloc<double>(vn);
-                D.y = h->dalloc<double>(vn);
-                if (o.nu_n > 2) { D.wn = h->dalloc<double>(vn); D.zn2 = h->dalloc<double>(vn); }
-            }
+            if (alloc_x) { D.x = h->dalloc<double>(ve); D.f = h->dalloc<double>(ve); }
+            D.r = h->dalloc<double>(ve);
+            D.z = o.nu_s > 2 ? h->dalloc<double>(ve) : D.r;   // r and z are never live together for nu_s <= 2
+            if (o.nu_s > 2) D.z2 = h->dalloc<double>(ve);
+            D.zn = h->dalloc<double>(vn);
+            D.y = h->dalloc<double>(vn);
+            if (o.nu_n > 2) { D.wn = h->dalloc<double>(vn); D.zn2 = h->dalloc<double>(vn); }
             max_partial = std::max(max_partial, (ve + 255) / 256);
             max_partial = std::max(max_partial, (size_t)st::residual_partials(D));
-            // the device owns the operators now; keep only the metadata on the host
+            return D;
+        };
+        for (int l = 0; l <= h->g0; ++l) {
+            const int cnt = (int)h->hl[l].tau.size() / P;
+            h->dl.push_back(build(l, h->rank * cnt, cnt, P == 1 && l == L - 1, l > 0));
+        }
+        if (P > 1 && h->rank == 0)
+            for (int l = h->g0; l < L; ++l) h->dg.push_back(build(l, 0, (int)h->hl[l].tau.size(), l == L - 1, true));
+        for (st::HostLevel &H : h->hl) {   // the device owns the operators now; keep the metadata
             H.M = H.K = H.Kn = H.GT = H.Pg = H.Rg = st::HostELL();
             std::vector<double>().swap(H.Ainv);
             std::vector<double>().swap(H.Pt);
@@ -414,11 +462,13 @@ int st_residual(st_handle *h, const double *x, const double *f, double *r, doubl
 
 int st_vcycle(st_handle *h, double *x, const double *f) {
     if (!h || !x || !f) return fail(1, "null argument");
-    ST_GUARD(vcycle(h, 0, x, f))
+    if (h->nranks > 1) return fail(1, "multi-rank handles run the V-cycle through the st_lv_* level operations");
+    ST_GUARD(vcycle(h, h->dl, 0, x, f))
 }
 
 int st_solve(st_handle *h, double *x, const double *f, double tol, int maxit, int *iters, double *hist) {
     if (!h || !x || !f || maxit < 0) return fail(1, "bad argument");
+    if (h->nranks > 1) return fail(1, "multi-rank handles solve through paper_1911_09548_b200.distributed");
     ST_GUARD({
         const double nf = std::sqrt(norm2_plain(h, f, vec_len(h->dl[0], h->Q)));
         int it = 0;
@@ -426,7 +476,7 @@ int st_solve(st_handle *h, double *x, const double *f, double tol, int maxit, in
             const double rel = std::sqrt(residual_norm2(h, x, f)) / nf;
             if (hist) hist[it] = rel;
             if (rel <= tol || it == maxit) break;
-            vcycle(h, 0, x, f);
+            vcycle(h, h->dl, 0, x, f);
         }
         if (iters) *iters = it;
     })
@@ -527,6 +577,134 @@ int st_host_matrix(const st_params *p, int level, int which, int *rows, int *wid
     }
 }
 
+static std::vector<DevLevel> &level_set(st_handle *h, int set) {
+    if (set == 0) return h->dl;
+    if (set == 1 && !h->dg.empty()) return h->dg;
+    throw std::invalid_argument("no such level set on this rank");
+}
+
+static DevLevel &level_of(st_handle *h, int set, int level) {
+    auto &V = level_set(h, set);
+    if (level < 0 || level >= (int)V.size()) throw std::invalid_argument("level out of range");
+    return V[level];
+}
+
+int st_lv_count(const st_handle *hc, int set, int *n) {
+    st_handle *h = const_cast<st_handle *>(hc);
+    if (!h || !n) return fail(1, "null argument");
+    *n = set == 0 ? (int)h->dl.size() : (set == 1 ? (int)h->dg.size() : 0);
+    return 0;
+}
+
+int st_lv_get(const st_handle *hc, int set, int level, st_level_t *out) {
+    st_handle *h = const_cast<st_handle *>(hc);
+    if (!h || !out) return fail(1, "null argument");
+    try {
+        DevLevel &L = level_of(h, set, level);
+        const int gl = set == 0 ? level : h->g0 + level;
+        std::memset(out, 0, sizeof(*out));
+        out->set = set; out->level = level; out->global_level = gl;
+        out->n_slabs = L.S;
+        out->slab0 = set == 0 ? h->rank * L.S : 0;
+        out->n_edges = L.n_edges; out->n_nodes = L.n_nodes; out->q = h->Q - 1;
+        out->coarsest = L.Ainv != nullptr;
+        out->space_coarsened = L.space_coarsened;
+        out->x = L.x; out->f = L.f; out->r = L.r;
+        return 0;
+    } catch (const std::exception &e) {
+        return fail(1, e.what());
+    }
+}
+
+int st_lv_residual(st_handle *h, int set, int level, const double *x, const double *f, const double *prev, double *r,
+                   double *norm2) {
+    if (!h || !x || !f) return fail(1, "null argument");
+    ST_GUARD({
+        DevLevel &L = level_of(h, set, level);
+        auto s = (st::Stream)h->stream;
+        const int Q = h->Q;
+        if (r) h->run("residual", 3 * evec(L, Q) + op_bytes(L), 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, prev, r, nullptr, h->o.omega_s, nullptr); });
+        if (norm2) {
+            int g = 0;
+            h->run("residual_norm", 2 * evec(L, Q) + op_bytes(L), 1,
+                   [&] { g = st::launch_residual(s, L, h->kt, Q, x, f, prev, nullptr, nullptr, h->o.omega_s, h->partial); });
+            h->run("reduce", 8.0 * g, 1, [&] { st::launch_reduce(s, g, h->partial, h->dscal); });
+            ck(cudaMemcpyAsync(norm2, h->dscal, sizeof(double), cudaMemcpyDeviceToHost, h->stream), "norm d2h");
+            ck(cudaStreamSynchronize(h->stream), "sync");
+        }
+    })
+}
+
+int st_lv_smooth_S(st_handle *h, int set, int level, double *x, const double *f, const double *prev) {
+    if (!h || !x || !f) return fail(1, "null argument");
+    ST_GUARD(smooth_S(h, level_of(h, set, level), x, f, prev))
+}
+
+int st_lv_correct_local(st_handle *h, int set, int level, double *x, const double *f, const double *prev, double *tot) {
+    if (!h || !x || !f) return fail(1, "null argument");
+    ST_GUARD(correct_A_local(h, level_of(h, set, level), x, f, prev, tot))
+}
+
+int st_lv_correct_apply(st_handle *h, int set, int level, double *x, const double *carry) {
+    if (!h || !x) return fail(1, "null argument");
+    ST_GUARD(correct_A_apply(h, level_of(h, set, level), x, carry))
+}
+
+int st_lv_restrict(st_handle *h, int set, int level, const double *r, double *fc) {
+    if (!h || !r || !fc) return fail(1, "null argument");
+    ST_GUARD({
+        auto &V = level_set(h, set);
+        if (level < 0 || level + 1 >= (int)V.size()) throw std::invalid_argument("no coarser level in this set");
+        restrict_to(h, V[level], V[level + 1], r, fc);
+    })
+}
+
+int st_lv_prolong(st_handle *h, int set, int level, const double *xc, double *x) {
+    if (!h || !xc || !x) return fail(1, "null argument");
+    ST_GUARD({
+        auto &V = level_set(h, set);
+        if (level < 0 || level + 1 >= (int)V.size()) throw std::invalid_argument("no coarser level in this set");
+        prolong_from(h, V[level], V[level + 1], xc, x);
+    })
+}
+
+int st_lv_vcycle(st_handle *h, int set, int level, double *x, const double *f) {
+    if (!h || !x || !f) return fail(1, "null argument");
+    ST_GUARD({
+        auto &V = level_set(h, set);
+        if (V.back().Ainv == nullptr) throw std::invalid_argument("this level set has no coarsest level");
+        if (level < 0 || level >= (int)V.size()) throw std::invalid_argument("level out of range");
+        vcycle(h, V, level, x, f);
+    })
+}
+
+int st_lv_end_values(st_handle *h, int set, int level, const double *x, double *out) {
+    if (!h || !x || !out) return fail(1, "null argument");
+    ST_GUARD({
+        DevLevel &L = level_of(h, set, level);
+        h->run("end_values", 16.0 * L.n_edges, 1, [&] { st::launch_end_values((st::Stream)h->stream, L.n_edges, h->Q, L.S, x, out); });
+    })
+}
+
+int st_copy_slabs(st_handle *h, int rows, int q, int ns, double *dst, int dS, int dk0, const double *src, int sS, int sk0,
+                  int add) {
+    if (!h || !dst || !src || rows < 0 || ns < 0 || dk0 < 0 || sk0 < 0 || dk0 + ns > dS || sk0 + ns > sS)
+        return fail(1, "bad argument");
+    ST_GUARD(h->run("copy_slabs", 16.0 * rows * (q + 1) * ns, 1, [&] {
+        st::launch_copy_slabs((st::Stream)h->stream, rows, q + 1, ns, dst, dS, dk0, src, sS, sk0, add != 0);
+    }))
+}
+
+int st_zero(st_handle *h, double *ptr, int64_t n) {
+    if (!h || (!ptr && n)) return fail(1, "null argument");
+    ST_GUARD(ck(cudaMemsetAsync(ptr, 0, sizeof(double) * (size_t)n, h->stream), "memset"))
+}
+
+int st_sync(st_handle *h) {
+    if (!h) return fail(1, "null handle");
+    ST_GUARD(ck(cudaStreamSynchronize(h->stream), "sync"))
+}
+
 int st_info(const st_handle *h, st_info_t *info) {
     if (!h || !info) return fail(1, "null argument");
     std::memset(info, 0, sizeof(*info));
@@ -540,7 +718,11 @@ int st_info(const st_handle *h, st_info_t *info) {
         info->level_space_coarsened[l] = h->hl[l].space_coarsened ? 1 : 0;
         info->level_lambda[l] = h->hl[l].lambda;
     }
-    for (int l = 0; l < info->n_levels; ++l) info->level_matrix_free[l] = h->dl[l].use_march ? 1 : 0;
+    for (int l = 0; l < info->n_levels; ++l) {
+        const DevLevel *D = l < (int)h->dl.size() ? &h->dl[l]
+                          : (l - h->g0 < (int)h->dg.size() ? &h->dg[l - h->g0] : nullptr);
+        info->level_matrix_free[l] = D && D->use_march ? 1 : 0;
+    }
     info->kernel_launches = h->launches;
     info->device_bytes = h->bytes;
     return 0;

@@ -126,7 +126,10 @@ void launch_node_sweep(Stream st, const DevLevel &L, int Q, const double *z, con
                        double *zout);
 void launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mode, const double *z,
                       const double *w, double omega_n, const double *carry, double *y, double *tot);
-void launch_g_update(Stream st, const DevLevel &L, int Q, const double *y, double *x);
+void launch_g_update(Stream st, const DevLevel &L, const KT &kt, int Q, const double *y, const double *carry, double *x);
+void launch_copy_slabs(Stream st, int rows, int Q, int ns, double *dst, int dS, int dk0, const double *src, int sS,
+                       int sk0, bool add);
+void launch_end_values(Stream st, int rows, int Q, int S, const double *x, double *out);
 void launch_restrict(Stream st, const DevLevel &F, const DevLevel &C, int Q, const double *r, double *fc);
 void launch_prolong(Stream st, const DevLevel &F, int Q, const double *xc, double *x);
 int launch_coarsest(Stream st, const DevLevel &L, int Q, const double *f, double *x);

@@ -559,15 +559,17 @@ __global__ void __launch_bounds__(kBlock) k_node_scan(int nodes, int S, DevELL K
     if (tot && lane == 0) tot[node] = carry;
 }
 
-// x += G y : x[e][a][k] += y[end][a][k] - y[start][a][k]
+// x += G (y + g carry) : x[e][a][k] += y[end][a][k] - y[start][a][k] + g_a (carry[end] - carry[start])
+// (carry: integrated end value before this slab block, R2; null = 0)
 template <int Q, int SPL>
 __global__ void __launch_bounds__(kBlock) k_g_update(BoxMap m, const int *__restrict__ en, const double *__restrict__ y,
-                                                     double *__restrict__ x) {
+                                                     const double *__restrict__ carry, KT kt, double *__restrict__ x) {
     box_loop(m, [&](int e, int k0, bool valid) {
     if (!valid) return;
     const int S = m.S;
     const int n0 = __ldg(en + 2 * e), n1 = __ldg(en + 2 * e + 1);
     const size_t QS = (size_t)Q * S;
+    const double dc = carry ? __ldg(carry + n1) - __ldg(carry + n0) : 0.0;
 #pragma unroll
     for (int a = 0; a < Q; ++a) {
         double y0[SPL], y1[SPL], xv[SPL];
@@ -575,12 +577,32 @@ __global__ void __launch_bounds__(kBlock) k_g_update(BoxMap m, const int *__rest
         ldv<SPL>(y + n1 * QS + a * S + k0, y1);
         ldv_rw<SPL>(x + e * QS + a * S + k0, xv);
 #pragma unroll
-        for (int j = 0; j < SPL; ++j) xv[j] += y1[j] - y0[j];
+        for (int j = 0; j < SPL; ++j) xv[j] += y1[j] - y0[j] + kt.g[a] * dc;
         stv<SPL>(x + e * QS + a * S + k0, xv);
     }
 });
 }
 
+// strided slab copy between space-time vectors with the same rows and Q:
+// dst[row][a][dk0 + s] (+)= src[row][a][sk0 + s], s < ns
+__global__ void __launch_bounds__(kBlock) k_copy_slabs(int rows, int Q, int ns, double *__restrict__ dst, int dS, int dk0,
+                                                       const double *__restrict__ src, int sS, int sk0, int add) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= (long long)rows * Q * ns) return;
+    const int s = (int)(i % ns);
+    const long long ra = i / ns;
+    const int a = (int)(ra % Q), row = (int)(ra / Q);
+    const double v = src[((long long)row * Q + a) * sS + sk0 + s];
+    double *d = dst + ((long long)row * Q + a) * dS + dk0 + s;
+    *d = add ? *d + v : v;
+}
+
+// out[row] = x[row][q][S-1] (the trace handed to the next rank)
+__global__ void __launch_bounds__(kBlock) k_end_values(int rows, int Q, int S, const double *__restrict__ x,
+                                                       double *__restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < rows) out[i] = x[((long long)i * Q + Q - 1) * S + S - 1];
+}
 
 // ------------------------------------------------ pencil march (uniform hex levels)
 // Grid: blocks ordered slab-chunk-major; block = 4 warps = 4 consecutive pencils (j, k)
@@ -1051,9 +1073,19 @@ void launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mod
     }));
 }
 
-void launch_g_update(Stream st, const DevLevel &L, int Q, const double *y, double *x) {
+void launch_g_update(Stream st, const DevLevel &L, const KT &kt, int Q, const double *y, const double *carry, double *x) {
     const BoxMap m = edge_map(L);
-    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, k_g_update<QQ, SP><<<grid(m), kBlock, 0, st>>>(m, L.edge_nodes, y, x)));
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, k_g_update<QQ, SP><<<grid(m), kBlock, 0, st>>>(m, L.edge_nodes, y, carry, kt, x)));
+}
+
+void launch_copy_slabs(Stream st, int rows, int Q, int ns, double *dst, int dS, int dk0, const double *src, int sS,
+                       int sk0, bool add) {
+    const long long n = (long long)rows * Q * ns;
+    if (n > 0) k_copy_slabs<<<nblocks(n), kBlock, 0, st>>>(rows, Q, ns, dst, dS, dk0, src, sS, sk0, add ? 1 : 0);
+}
+
+void launch_end_values(Stream st, int rows, int Q, int S, const double *x, double *out) {
+    k_end_values<<<nblocks(rows), kBlock, 0, st>>>(rows, Q, S, x, out);
 }
 
 void launch_restrict(Stream st, const DevLevel &F, const DevLevel &C, int Q, const double *r, double *fc) {

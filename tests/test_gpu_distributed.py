@@ -1,0 +1,105 @@
+"""The multi-rank driver (paper_1911_09548_b200.distributed) with the CUDA level operations.
+
+P = 1: the driver sequences the same kernels as st_vcycle -> bitwise equal result.
+P = 2: two processes on the one GPU of this box with gloo messages staged through host memory
+(no kernel ever waits on another process); each builds a multi-rank handle (its slab block,
+rank 0 also the gathered coarse levels) and the gathered result must equal the single-process
+V-cycle to rounding."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _inputs(w, seed=5):
+    rng = np.random.default_rng(seed)
+    F = workloads.from_oracle(rng.uniform(-1, 1, (w.S, w.q + 1, w.n_edges)))
+    X0 = workloads.from_oracle(rng.uniform(-1, 1, (w.S, w.q + 1, w.n_edges)))
+    return X0, F
+
+
+@pytest.mark.parametrize("name", ["c1", "c5", "c2"])
+def test_driver_single_rank_bitwise(name):
+    import paper_1911_09548_b200 as p
+    from paper_1911_09548_b200.distributed import DistributedVCycle, GpuOps, LocalComm
+    p.build.build()
+    w = workloads.small(name)
+    X0, F = _inputs(w)
+    s = p.Solver.from_workload(w)
+    xa = torch.from_numpy(X0).cuda()
+    f = torch.from_numpy(F).cuda()
+    xb = xa.clone()
+    s.vcycle(xa, f)
+    DistributedVCycle(GpuOps(s), LocalComm()).vcycle(xb, f)
+    torch.cuda.synchronize()
+    assert torch.equal(xa, xb)
+
+
+def _worker(rank, P, port, name, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    try:
+        import paper_1911_09548_b200 as p
+        from paper_1911_09548_b200.distributed import DistributedVCycle, GpuOps, TorchComm
+        torch.cuda.set_device(0)
+        w = workloads.small(name)
+        X0, F = _inputs(w)
+        s = p.Solver.from_workload(w, rank=rank, nranks=P)
+        cnt = w.S // P
+        x = torch.from_numpy(np.ascontiguousarray(X0[:, :, rank * cnt:(rank + 1) * cnt])).cuda()
+        f = torch.from_numpy(np.ascontiguousarray(F[:, :, rank * cnt:(rank + 1) * cnt])).cuda()
+        drv = DistributedVCycle(GpuOps(s), TorchComm())
+        drv.vcycle(x, f)
+        torch.cuda.synchronize()
+        parts = drv.comm.gather_to_root(x)
+        x.zero_()
+        it, hist = drv.solve(x, f, tol=1e-10, maxit=5)
+        if rank == 0:
+            out.put((torch.cat([q.cpu() for q in parts], dim=2).numpy(), hist))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,P", [("c1", 2), ("c4", 2), ("c5", 2), ("c1", 4)])
+def test_two_ranks_one_gpu(name, P):
+    import torch.multiprocessing as mp
+    import paper_1911_09548_b200 as p
+    p.build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, P, port, name, q)) for r in range(P)]
+    for pr in procs:
+        pr.start()
+    Xd, hist = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    w = workloads.small(name)
+    X0, F = _inputs(w)
+    s = p.Solver.from_workload(w)
+    x = torch.from_numpy(X0).cuda()
+    f = torch.from_numpy(F).cuda()
+    s.vcycle(x, f)
+    Xs = x.cpu().numpy()
+    tol = 1e-11 if name == "c5" else 1e-12
+    assert np.linalg.norm(Xd - Xs) <= tol * np.linalg.norm(Xs)
+    x.zero_()
+    it, h1 = s.solve(x, f, tol=1e-10, maxit=5)
+    np.testing.assert_allclose(hist, h1, rtol=1e-10, atol=1e-14)
