@@ -36,7 +36,8 @@ def _inputs(w, seed=5):
 def test_driver_single_rank_bitwise(name):
     import paper_1911_09548_b200 as p
     from paper_1911_09548_b200.distributed import DistributedVCycle, GpuOps, LocalComm
-    p.build.build()
+    from paper_1911_09548_b200 import build as _b
+    _b.build()
     w = workloads.small(name)
     X0, F = _inputs(w)
     s = p.Solver.from_workload(w)
@@ -80,7 +81,8 @@ def _worker(rank, P, port, name, out):
 def test_two_ranks_one_gpu(name, P):
     import torch.multiprocessing as mp
     import paper_1911_09548_b200 as p
-    p.build.build()
+    from paper_1911_09548_b200 import build as _b
+    _b.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
