@@ -37,6 +37,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-out", default=None, help="write per-kernel event stats (json)")
+    ap.add_argument("--kernel-path", type=int, default=0, help="0: matrix-free march on uniform levels, 1: ELL")
     return ap.parse_args()
 
 
@@ -168,7 +169,7 @@ def run_ours(args, rank, world, local_rank):
     w = workloads.c4(n=args.n, S=args.slabs * world, tau=1.0 / 4096)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        s = p.Solver.from_workload(w, stream=stream, rank=rank, nranks=world)
+        s = p.Solver.from_workload(w, stream=stream, rank=rank, nranks=world, kernel_path=args.kernel_path)
         g = torch.Generator(device="cuda")
         g.manual_seed(3 + 1000 * rank)
         f = torch.empty(s.shape, dtype=torch.float64, device="cuda").uniform_(-1.0, 1.0, generator=g)

@@ -361,7 +361,8 @@ int st_setup(const st_params *p, st_handle **out) {
             D.nbox_e = (int)H.bptr_e.size() - 1; D.nbox_n = (int)H.bptr_n.size() - 1;
             D.tau = h->upload(std::vector<double>(H.tau.begin() + b, H.tau.begin() + b + cnt));
             D.space_coarsened = H.space_coarsened;
-            if (H.uniform && o.kernel_path == 0 && Q <= 2) {
+            // the march uses 32-bit element offsets
+            if (H.uniform && o.kernel_path == 0 && Q <= 2 && (long long)H.mesh.n_edges * Q * cnt < (1LL << 31)) {
                 const double hx = H.hbox[0], hy = H.hbox[1], hz = H.hbox[2];
                 D.use_march = true;
                 D.grid.nx = H.mesh.n[0]; D.grid.ny = H.mesh.n[1]; D.grid.nz = H.mesh.n[2];
