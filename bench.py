@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-out", default=None, help="write per-kernel event stats (json)")
-    ap.add_argument("--kernel-path", type=int, default=0, help="0: matrix-free march on uniform levels, 1: ELL")
+    ap.add_argument("--kernel-path", type=int, default=0, help="0: assembled ELL (default), 1: matrix-free march")
     return ap.parse_args()
 
 

@@ -70,8 +70,8 @@ typedef struct st_params {
     double lambda_crit;    /* Eq. (3) threshold, default 0.1 (l.292) */
     int mode;              /* 0 auto (Eq. 3 per level), 1 semi-time only, 2 full at the top level only (Table 1) */
     int min_slabs;         /* stop time coarsening at this many slabs, default 1 */
-    int kernel_path;       /* 0: matrix-free pencil march on uniform hex levels, ELL elsewhere
-                              (default); 1: assembled ELL operators everywhere */
+    int kernel_path;       /* 0: assembled ELL operators on every level (default, fastest
+                              measured); 1: matrix-free pencil march on uniform hex levels */
     int rank, nranks;      /* multi-GPU (one process per GPU): nranks <= 1 means single GPU.
                               With nranks > 1, tau is the GLOBAL slab array; this rank owns the
                               contiguous block [rank*n_slabs/nranks, (rank+1)*n_slabs/nranks)

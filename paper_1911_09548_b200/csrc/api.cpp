@@ -362,7 +362,7 @@ int st_setup(const st_params *p, st_handle **out) {
             D.tau = h->upload(std::vector<double>(H.tau.begin() + b, H.tau.begin() + b + cnt));
             D.space_coarsened = H.space_coarsened;
             // the march uses 32-bit element offsets
-            if (H.uniform && o.kernel_path == 0 && Q <= 2 && (long long)H.mesh.n_edges * Q * cnt < (1LL << 31)) {
+            if (H.uniform && o.kernel_path == 1 && Q <= 2 && (long long)H.mesh.n_edges * Q * cnt < (1LL << 31)) {
                 const double hx = H.hbox[0], hy = H.hbox[1], hz = H.hbox[2];
                 D.use_march = true;
                 D.grid.nx = H.mesh.n[0]; D.grid.ny = H.mesh.n[1]; D.grid.nz = H.mesh.n[2];

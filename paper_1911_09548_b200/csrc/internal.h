@@ -105,7 +105,7 @@ struct Options {
     double lambda_crit = 0.1;
     int mode = 0;
     int min_slabs = 1;
-    int kernel_path = 0;    // 0: matrix-free march on uniform hex levels, ELL elsewhere; 1: ELL only
+    int kernel_path = 0;    // 0: assembled ELL operators (default); 1: matrix-free pencil march on uniform hex levels
 };
 
 // kernel-side time constants (passed by value to kernels)

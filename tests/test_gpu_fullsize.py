@@ -35,12 +35,12 @@ def sampled_residual(w, X_rows, F_rows, rows, M, K):
     return np.array(out)
 
 
-@pytest.mark.parametrize("name", ["c4", "c3", "c5"])
-def test_fullsize_residual_sampled(torch_cuda, name):
+@pytest.mark.parametrize("name,path", [("c4", 0), ("c4", 1), ("c3", 0), ("c5", 0)])
+def test_fullsize_residual_sampled(torch_cuda, name, path):
     torch = torch_cuda
     import paper_1911_09548_b200 as p
     w = {"c4": lambda: workloads.c4(), "c3": lambda: workloads.c3(), "c5": lambda: workloads.c5()}[name]()
-    s = p.Solver.from_workload(w)
+    s = p.Solver.from_workload(w, kernel_path=path)
     g = torch.Generator(device="cuda")
     g.manual_seed(7)
     x = torch.empty(s.shape, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g)

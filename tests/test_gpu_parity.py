@@ -112,8 +112,8 @@ def test_vcycle_parity_random_start(torch_cuda, name, q):
 @pytest.mark.parametrize("name", ["c1", "c4", "c3"])
 @pytest.mark.parametrize("q", [0, 1, 2])
 def test_march_matches_ell_and_oracle(torch_cuda, name, q):
-    # uniform hex levels run the matrix-free pencil march; the assembled-ELL path (kernel_path=1)
-    # and the oracle must give the same V-cycle
+    # kernel_path=1 runs the matrix-free pencil march on uniform hex levels; it and the default
+    # assembled-ELL path must give the oracle's V-cycle
     torch = torch_cuda
     w = workloads.small(name)
     w.q = q
