@@ -361,6 +361,7 @@ int st_setup(const st_params *p, st_handle **out) {
             D.nbox_e = (int)H.bptr_e.size() - 1; D.nbox_n = (int)H.bptr_n.size() - 1;
             D.tau = h->upload(std::vector<double>(H.tau.begin() + b, H.tau.begin() + b + cnt));
             D.space_coarsened = H.space_coarsened;
+            if (const char *e = std::getenv("ST_EDGE_LPR")) D.lpr_log2 = std::max(0, std::min(5, std::atoi(e)));
             // the march uses 32-bit element offsets
             if (H.uniform && o.kernel_path == 1 && Q <= 2 && (long long)H.mesh.n_edges * Q * cnt < (1LL << 31)) {
                 const double hx = H.hbox[0], hy = H.hbox[1], hz = H.hbox[2];

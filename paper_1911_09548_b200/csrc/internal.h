@@ -84,6 +84,7 @@ struct DevLevel {
     int *sched_e = nullptr, *bptr_e = nullptr, *sched_n = nullptr, *bptr_n = nullptr;
     int nbox_e = 0, nbox_n = 0;
     bool use_march = false;
+    int lpr_log2 = 5;       // edge kernels: log2(lanes per row); slab chunk = 2 << lpr_log2 (32: measured best)
     Grid3 grid{};
     double *tau = nullptr;
     double *Pt = nullptr;

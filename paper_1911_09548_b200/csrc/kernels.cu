@@ -942,7 +942,7 @@ static BoxMap make_boxmap(int S, const int *sched, const int *bptr, int n_boxes,
     return m;
 }
 static inline int grid(const BoxMap &m) { return m.n_boxes * ((m.S + m.chunk - 1) / m.chunk); }
-static inline BoxMap edge_map(const DevLevel &L) { return make_boxmap(L.S, L.sched_e, L.bptr_e, L.nbox_e); }
+static inline BoxMap edge_map(const DevLevel &L) { return make_boxmap(L.S, L.sched_e, L.bptr_e, L.nbox_e, L.lpr_log2); }
 static inline BoxMap node_map(const DevLevel &L) { return make_boxmap(L.S, L.sched_n, L.bptr_n, L.nbox_n); }
 
 #define ST_DISPATCH_Q(Q, ...)                                   \
