@@ -173,8 +173,9 @@ void correct_A_local(st_handle *h, DevLevel &L, double *x, const double *f, cons
     auto s = (st::Stream)h->stream;
     const int Q = h->Q;
     const double ev = evec(L, Q), nv = nvec(L, Q), kb = ell_bytes(L.Kn) + 8.0 * L.n_nodes;
-    h->run("residual", 3 * ev + op_bytes(L), 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, prev, L.r, nullptr, o.omega_s, nullptr); });
-    h->run("gt", ev + (o.nu_n > 2 ? 2 : 1) * nv + 8.0 * L.n_nodes, 1, [&] { st::launch_gt(s, L, Q, L.r, o.omega_n, L.zn, o.nu_n > 2 ? L.wn : nullptr); });
+    // fused nodal residual: w = G^T (f - L x) by a node-row SpMV with G^T M (K G = 0), zn = omega_n w / d_n
+    h->run("gtr", 2 * ev + (o.nu_n > 2 ? 2 : 1) * nv + ell_bytes(L.GtM) + 8.0 * L.n_nodes, 1,
+           [&] { st::launch_gtr(s, L, h->kt, Q, x, f, prev, o.omega_n, L.zn, o.nu_n > 2 ? L.wn : nullptr); });
     double *cur = L.zn, *other = L.zn2;
     int mode = o.nu_n == 1 ? 0 : (o.nu_n == 2 ? 1 : 2);
     for (int i = 2; i < o.nu_n; ++i) {
@@ -354,6 +355,7 @@ int st_setup(const st_params *p, st_handle **out) {
             if ((long long)D.n_edges * D.S >= (1LL << 31) || (long long)D.n_nodes * 32 >= (1LL << 31))
                 throw Unsupported("level too large for 32-bit thread indexing");
             D.M = h->upload(H.M); D.K = h->upload(H.K); D.Kn = h->upload(H.Kn); D.GT = h->upload(H.GT);
+            D.GtM = h->upload(H.GtM);
             D.dM = h->upload(H.dM); D.dK = h->upload(H.dK); D.dN = h->upload(H.dN);
             D.edge_nodes = h->upload(H.mesh.edge_nodes);
             D.sched_e = h->upload(H.sched_e); D.bptr_e = h->upload(H.bptr_e);
@@ -402,7 +404,7 @@ int st_setup(const st_params *p, st_handle **out) {
         if (P > 1 && h->rank == 0)
             for (int l = h->g0; l < L; ++l) h->dg.push_back(build(l, 0, (int)h->hl[l].tau.size(), l == L - 1, true));
         for (st::HostLevel &H : h->hl) {   // the device owns the operators now; keep the metadata
-            H.M = H.K = H.Kn = H.GT = H.Pg = H.Rg = st::HostELL();
+            H.M = H.K = H.Kn = H.GT = H.Pg = H.Rg = H.GtM = st::HostELL();
             std::vector<double>().swap(H.Ainv);
             std::vector<double>().swap(H.Pt);
             std::vector<int>().swap(H.mesh.cell_edges);

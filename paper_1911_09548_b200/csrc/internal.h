@@ -56,6 +56,7 @@ struct HostLevel {
     HostELL M, K, Kn;
     std::vector<double> dM, dK, dN;             // diagonals
     HostELL GT;                                 // node -> signed incident edges: col = 2*e + (sign<0), -1 pad
+    HostELL GtM;                                // G^T M_sigma (nodes x edges): the nodal residual operator
     double lambda = 0;                          // Eq. (3) value of this level
     bool space_coarsened = false;               // this -> next
     HostELL Pg;                                 // fine edge -> coarse edges (prolongation rows)
@@ -78,7 +79,7 @@ struct Grid3 {
 
 struct DevLevel {
     int n_edges = 0, n_nodes = 0, S = 0, Q = 1;
-    DevELL M, K, Kn, GT, Pg, Rg;
+    DevELL M, K, Kn, GT, Pg, Rg, GtM;
     double *dM = nullptr, *dK = nullptr, *dN = nullptr;
     int *edge_nodes = nullptr;
     int *sched_e = nullptr, *bptr_e = nullptr, *sched_n = nullptr, *bptr_n = nullptr;
@@ -123,6 +124,8 @@ void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, 
                   const double *r, double *out, double omega_s, double omega);
 void launch_axpy(Stream st, size_t n, double alpha, const double *z, double *x);
 void launch_gt(Stream st, const DevLevel &L, int Q, const double *r, double omega_n, double *zn, double *w);
+void launch_gtr(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f, const double *prev,
+                double omega_n, double *zn, double *w);
 void launch_node_sweep(Stream st, const DevLevel &L, int Q, const double *z, const double *w, double omega_n,
                        double *zout);
 void launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mode, const double *z,

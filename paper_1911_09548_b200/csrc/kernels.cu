@@ -415,6 +415,94 @@ __global__ void __launch_bounds__(kBlock) k_gt(BoxMap m, DevELL GT, const double
 });
 }
 
+
+// Fused nodal residual (first half of Eq. 5): w = G^T (f - L x) computed per node without the
+// edge residual: G^T K = 0, so w = G^T f - sum_a Ct[b][a] (G^T M x_a) + e_0 (G^T M x_q)(k-1);
+// zn = omega_n w / d_n is the first Jacobi sweep on K_n (w stored for nu_n > 2).
+template <int Q, int SPL, bool W_OUT>
+__global__ void __launch_bounds__(kBlock) k_gtr(BoxMap m, DevELL GT, DevELL GtM, const double *__restrict__ x,
+                                                const double *__restrict__ f, const double *__restrict__ prev,
+                                                const double *__restrict__ dN, double omega_n, KT kt,
+                                                double *__restrict__ zn, double *__restrict__ w) {
+    box_loop(m, [&](int node, int k0, bool valid) {
+        const int S = m.S;
+        const size_t QS = (size_t)Q * S;
+        double gm[Q][SPL];
+#pragma unroll
+        for (int a = 0; a < Q; ++a)
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) gm[a][j] = 0.0;
+        const Ent *e = GtM.e + (size_t)node * GtM.width;
+#pragma unroll 6
+        for (int s = 0; s < GtM.width; ++s) {
+            double v; int c;
+            ld_ent(e + s, v, c);
+            const double *xc = x + (size_t)c * QS + k0;
+#pragma unroll
+            for (int a = 0; a < Q; ++a) {
+                double xv[SPL];
+                ldv<SPL>(xc + a * S, xv);
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) gm[a][j] = fma(v, xv[j], gm[a][j]);
+            }
+        }
+        // coupling: (G^T M x_q) at slab k-1, from the previous lane of the row group or explicit
+        const int lpr = 1 << m.lpr_log2;
+        double mp[SPL];
+#pragma unroll
+        for (int j = 1; j < SPL; ++j) mp[j] = gm[Q - 1][j - 1];
+        const double up = __shfl_up_sync(0xffffffffu, gm[Q - 1][SPL - 1], 1, lpr);
+        if (((threadIdx.x & 31) & (lpr - 1)) != 0) {
+            mp[0] = up;
+        } else {
+            double acc = 0.0;
+            for (int s = 0; s < GtM.width; ++s) {
+                double v; int c;
+                ld_ent(e + s, v, c);
+                const double xp = k0 > 0 ? __ldg(x + (size_t)c * QS + (Q - 1) * S + k0 - 1) : (prev ? __ldg(prev + c) : 0.0);
+                acc = fma(v, xp, acc);
+            }
+            mp[0] = acc;
+        }
+        if (!valid) return;
+        double gf[Q][SPL];
+#pragma unroll
+        for (int a = 0; a < Q; ++a)
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) gf[a][j] = 0.0;
+        const int *gc = GT.col + (size_t)node * GT.width;
+        for (int s = 0; s < GT.width; ++s) {
+            const int code = __ldg(gc + s);
+            if (code < 0) break;
+            const double sg = (code & 1) ? -1.0 : 1.0;
+            const double *fe = f + (size_t)(code >> 1) * QS + k0;
+#pragma unroll
+            for (int a = 0; a < Q; ++a) {
+                double fv[SPL];
+                ldv<SPL>(fe + a * S, fv);
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) gf[a][j] = fma(sg, fv[j], gf[a][j]);
+            }
+        }
+        const double inv = omega_n / __ldg(dN + node);
+        const size_t base = (size_t)node * QS + k0;
+#pragma unroll
+        for (int b = 0; b < Q; ++b) {
+            double wv[SPL], zv[SPL];
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) {
+                double acc = 0.0;
+#pragma unroll
+                for (int a = 0; a < Q; ++a) acc += kt.Ct[b * Q + a] * gm[a][j];
+                wv[j] = gf[b][j] - acc + (b == 0 ? mp[j] : 0.0);
+                zv[j] = wv[j] * inv;
+            }
+            stv<SPL>(zn + base + b * S, zv);
+            if (W_OUT) stv<SPL>(w + base + b * S, wv);
+        }
+    });
+}
+
 // middle nodal sweep: zout = z + omega_n (w - K_n z)/dN
 template <int Q, int SPL>
 __global__ void __launch_bounds__(kBlock) k_node_sweep(BoxMap m, DevELL Kn, const double *__restrict__ dN,
@@ -1053,6 +1141,15 @@ void launch_gt(Stream st, const DevLevel &L, int Q, const double *r, double omeg
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, {
         if (w) k_gt<QQ, SP, true><<<grid(m), kBlock, 0, st>>>(m, L.GT, r, L.dN, omega_n, zn, w);
         else k_gt<QQ, SP, false><<<grid(m), kBlock, 0, st>>>(m, L.GT, r, L.dN, omega_n, zn, w);
+    }));
+}
+
+void launch_gtr(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f, const double *prev,
+                double omega_n, double *zn, double *w) {
+    const BoxMap m = make_boxmap(L.S, L.sched_n, L.bptr_n, L.nbox_n, L.lpr_log2);
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, {
+        if (w) k_gtr<QQ, SP, true><<<grid(m), kBlock, 0, st>>>(m, L.GT, L.GtM, x, f, prev, L.dN, omega_n, kt, zn, w);
+        else k_gtr<QQ, SP, false><<<grid(m), kBlock, 0, st>>>(m, L.GT, L.GtM, x, f, prev, L.dN, omega_n, kt, zn, w);
     }));
 }
 

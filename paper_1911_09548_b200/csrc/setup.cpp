@@ -423,6 +423,21 @@ void assemble(HostLevel &L) {
         for (size_t s = 0; s < cs.size(); ++s) GT.col[(size_t)r * GT.width + s] = cs[s];
     }
     L.GT = GT;
+    // G^T M_sigma: since K G = 0, G^T (f - L x) = G^T f - (Ct (x) G^T M) x + (Nt (x) G^T M) x_prev
+    // (fused nodal residual)
+    RowAcc gm(m.n_nodes, GT.width * L.M.width);
+    for (int n = 0; n < m.n_nodes; ++n)
+        for (int s = 0; s < GT.width; ++s) {
+            const int code = GT.col[(size_t)n * GT.width + s];
+            if (code < 0) break;
+            const int e = code >> 1;
+            const double sg = (code & 1) ? -1.0 : 1.0;
+            for (int t = 0; t < L.M.width; ++t) {
+                const double v = L.M.val[(size_t)e * L.M.width + t];
+                if (v != 0.0) gm.add(n, L.M.col[(size_t)e * L.M.width + t], sg * v);
+            }
+        }
+    L.GtM = gm.finish(false);
 }
 
 // ------------------------------------------------------------- transfers
