@@ -356,6 +356,13 @@ int st_setup(const st_params *p, st_handle **out) {
                 throw Unsupported("level too large for 32-bit thread indexing");
             D.M = h->upload(H.M); D.K = h->upload(H.K); D.Kn = h->upload(H.Kn); D.GT = h->upload(H.GT);
             D.GtM = h->upload(H.GtM);
+            {
+                std::vector<double2> mkv(H.MK.val.size());
+                for (size_t i = 0; i < mkv.size(); ++i) mkv[i] = make_double2(H.MK.val[i], H.MKk[i]);
+                D.mk_width = H.MK.width;
+                D.mk_col = h->upload(H.MK.col);
+                D.mk_val = h->upload(mkv);
+            }
             D.dM = h->upload(H.dM); D.dK = h->upload(H.dK); D.dN = h->upload(H.dN);
             D.edge_nodes = h->upload(H.mesh.edge_nodes);
             D.sched_e = h->upload(H.sched_e); D.bptr_e = h->upload(H.bptr_e);
@@ -404,7 +411,8 @@ int st_setup(const st_params *p, st_handle **out) {
         if (P > 1 && h->rank == 0)
             for (int l = h->g0; l < L; ++l) h->dg.push_back(build(l, 0, (int)h->hl[l].tau.size(), l == L - 1, true));
         for (st::HostLevel &H : h->hl) {   // the device owns the operators now; keep the metadata
-            H.M = H.K = H.Kn = H.GT = H.Pg = H.Rg = H.GtM = st::HostELL();
+            H.M = H.K = H.Kn = H.GT = H.Pg = H.Rg = H.GtM = H.MK = st::HostELL();
+            std::vector<double>().swap(H.MKk);
             std::vector<double>().swap(H.Ainv);
             std::vector<double>().swap(H.Pt);
             std::vector<int>().swap(H.mesh.cell_edges);

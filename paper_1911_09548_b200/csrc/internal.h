@@ -4,6 +4,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "../../include/st.h"
 
 namespace st {
@@ -57,6 +59,8 @@ struct HostLevel {
     std::vector<double> dM, dK, dN;             // diagonals
     HostELL GT;                                 // node -> signed incident edges: col = 2*e + (sign<0), -1 pad
     HostELL GtM;                                // G^T M_sigma (nodes x edges): the nodal residual operator
+    HostELL MK;                                 // merged pattern of M and K: col, val = M entry, valK = K entry
+    std::vector<double> MKk;
     double lambda = 0;                          // Eq. (3) value of this level
     bool space_coarsened = false;               // this -> next
     HostELL Pg;                                 // fine edge -> coarse edges (prolongation rows)
@@ -80,6 +84,9 @@ struct Grid3 {
 struct DevLevel {
     int n_edges = 0, n_nodes = 0, S = 0, Q = 1;
     DevELL M, K, Kn, GT, Pg, Rg, GtM;
+    int mk_width = 0;
+    int *mk_col = nullptr;          // [row][slot] union columns of M and K
+    double2 *mk_val = nullptr;      // [row][slot] (M value, K value)
     double *dM = nullptr, *dK = nullptr, *dN = nullptr;
     int *edge_nodes = nullptr;
     int *sched_e = nullptr, *bptr_e = nullptr, *sched_n = nullptr, *bptr_n = nullptr;

@@ -205,6 +205,43 @@ __device__ __forceinline__ void spatial_apply(const DevELL &M, const DevELL &K, 
     }
 }
 
+// Merged M/K ELL: one column list, (M value, K value) pairs; one gather feeds both products.
+struct MKELL {
+    const int *col;
+    const double2 *val;
+    int width;
+};
+
+template <int Q, int SPL, int W>
+__device__ __forceinline__ void spatial_apply_mk(const MKELL &A, int row, int k0, int S,
+                                                 const double *__restrict__ x,
+                                                 double (&mx)[Q][SPL], double (&kx)[Q][SPL]) {
+    const size_t QS = (size_t)Q * S;
+#pragma unroll
+    for (int a = 0; a < Q; ++a)
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) { mx[a][j] = 0.0; kx[a][j] = 0.0; }
+    const int w = W > 0 ? W : A.width;
+    const int *cc = A.col + (size_t)row * w;
+    const double2 *vv = A.val + (size_t)row * w;
+#pragma unroll (W > 0 ? W : 3)
+    for (int s = 0; s < w; ++s) {
+        const int c = __ldg(cc + s);
+        const double2 v = __ldg(vv + s);
+        const double *xc = x + (size_t)c * QS + k0;
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+            double xv[SPL];
+            ldv<SPL>(xc + a * S, xv);
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) {
+                mx[a][j] = fma(v.x, xv[j], mx[a][j]);
+                kx[a][j] = fma(v.y, xv[j], kx[a][j]);
+            }
+        }
+    }
+}
+
 // Upwind coupling (Nt (x) M) x_{k-1} = e_0 (M x)[q][k-1]: the previous slab's M-image
 // is the own lane's (j >= 1) or the previous lane's (j = 0) already computed mx[q];
 // only the first lane of a row group (k0 at a chunk start) gathers it explicitly.
@@ -243,7 +280,7 @@ __device__ __forceinline__ void coupling(const DevELL &M, int row, int k0, int S
 // r = f - L x; optionally z = omega_s D^{-1} r (first Jacobi sweep of B from zero)
 // and per-block partial sums of |r|^2.
 template <int Q, int SPL, int WM, int WK, bool R_OUT, bool Z_OUT, bool NORM>
-__global__ void __launch_bounds__(kBlock) k_residual(BoxMap m, DevELL M, DevELL K, const double *__restrict__ tau,
+__global__ void __launch_bounds__(kBlock) k_residual(BoxMap m, DevELL M, MKELL MK, const double *__restrict__ tau,
                                                      const double *__restrict__ x, const double *__restrict__ f,
                                                      const double *__restrict__ prev, double *__restrict__ r,
                                                      double *__restrict__ z, const double *__restrict__ dM,
@@ -253,7 +290,7 @@ __global__ void __launch_bounds__(kBlock) k_residual(BoxMap m, DevELL M, DevELL 
     box_loop(m, [&](int row, int k0, bool valid) {
         const int S = m.S;
         double mx[Q][SPL], kx[Q][SPL], mp[SPL];
-        spatial_apply<Q, SPL, WM, WK>(M, K, row, k0, S, x, mx, kx);
+        spatial_apply_mk<Q, SPL, WK>(MK, row, k0, S, x, mx, kx);
         coupling<Q, SPL, WM>(M, row, k0, S, 1 << m.lpr_log2, x, prev, mx, mp);
         if (!valid) return;
         double t[SPL];
@@ -309,14 +346,14 @@ __global__ void __launch_bounds__(kBlock) k_residual(BoxMap m, DevELL M, DevELL 
 // LAST: x += omega * znew (the smoother update of Eq. 2), in place (x is only
 // read at its own row).
 template <int Q, int SPL, int WM, int WK, bool LAST, bool RECON>
-__global__ void __launch_bounds__(kBlock) k_sweep(BoxMap m, DevELL M, DevELL K, const double *__restrict__ tau,
+__global__ void __launch_bounds__(kBlock) k_sweep(BoxMap m, DevELL M, MKELL MK, const double *__restrict__ tau,
                                                   const double *__restrict__ dM, const double *__restrict__ dK,
                                                   const double *__restrict__ z, const double *__restrict__ r,
                                                   double *out, double omega_s, double omega, KT kt) {
     box_loop(m, [&](int row, int k0, bool valid) {
     const int S = m.S;
     double mz[Q][SPL], kz[Q][SPL];
-    spatial_apply<Q, SPL, WM, WK>(M, K, row, k0, S, z, mz, kz);
+    spatial_apply_mk<Q, SPL, WK>(MK, row, k0, S, z, mz, kz);
     if (!valid) return;
     double t[SPL];
     ldv<SPL>(tau + k0, t);
@@ -1090,16 +1127,17 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
     }
     const BoxMap m = edge_map(L);
     const int g = grid(m);
-    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.K.width, {
+    const MKELL MK{L.mk_col, L.mk_val, L.mk_width};
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.mk_width, {
         if (partial) {
-            if (r) k_residual<QQ, SP, WM_, WK_, true, false, true><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
-            else k_residual<QQ, SP, WM_, WK_, false, false, true><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            if (r) k_residual<QQ, SP, WM_, WK_, true, false, true><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            else k_residual<QQ, SP, WM_, WK_, false, false, true><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         } else if (r && z) {
-            k_residual<QQ, SP, WM_, WK_, true, true, false><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            k_residual<QQ, SP, WM_, WK_, true, true, false><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         } else if (z) {
-            k_residual<QQ, SP, WM_, WK_, false, true, false><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            k_residual<QQ, SP, WM_, WK_, false, true, false><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         } else {
-            k_residual<QQ, SP, WM_, WK_, true, false, false><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            k_residual<QQ, SP, WM_, WK_, true, false, false><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         }
     })));
     return g;
@@ -1124,11 +1162,12 @@ void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, 
     }
     const BoxMap m = edge_map(L);
     const int g = grid(m);
-    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.K.width, {
-        if (last && recon) k_sweep<QQ, SP, WM_, WK_, true, true><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
-        else if (last) k_sweep<QQ, SP, WM_, WK_, true, false><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
-        else if (recon) k_sweep<QQ, SP, WM_, WK_, false, true><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
-        else k_sweep<QQ, SP, WM_, WK_, false, false><<<g, kBlock, 0, st>>>(m, L.M, L.K, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+    const MKELL MK{L.mk_col, L.mk_val, L.mk_width};
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.mk_width, {
+        if (last && recon) k_sweep<QQ, SP, WM_, WK_, true, true><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+        else if (last) k_sweep<QQ, SP, WM_, WK_, true, false><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+        else if (recon) k_sweep<QQ, SP, WM_, WK_, false, true><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+        else k_sweep<QQ, SP, WM_, WK_, false, false><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
     })));
 }
 

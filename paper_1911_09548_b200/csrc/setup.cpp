@@ -403,6 +403,41 @@ void assemble(HostLevel &L) {
     L.M = M.finish(true);
     L.K = K.finish(true);
     L.Kn = Kn.finish(true);
+    // merged M/K pattern (one gather feeds both products)
+    {
+        RowAcc mk(m.n_edges, L.M.width + L.K.width), kk(m.n_edges, L.M.width + L.K.width);
+        for (int r = 0; r < m.n_edges; ++r) {
+            for (int s = 0; s < L.K.width; ++s) {
+                const double v = L.K.val[(size_t)r * L.K.width + s];
+                if (v != 0.0) { mk.add(r, L.K.col[(size_t)r * L.K.width + s], 0.0); kk.add(r, L.K.col[(size_t)r * L.K.width + s], v); }
+            }
+            for (int s = 0; s < L.M.width; ++s) {
+                const double v = L.M.val[(size_t)r * L.M.width + s];
+                if (v != 0.0) { mk.add(r, L.M.col[(size_t)r * L.M.width + s], v); kk.add(r, L.M.col[(size_t)r * L.M.width + s], 0.0); }
+            }
+        }
+        // same insertion order in both accumulators -> identical column lists; keep every slot
+        // (a zero M value must not drop a K entry), sorted by column
+        const int cap = mk.cap;
+        int width = 0;
+        for (int r = 0; r < m.n_edges; ++r) width = std::max(width, mk.cnt[r]);
+        L.MK.rows = m.n_edges; L.MK.width = std::max(width, 1);
+        L.MK.col.assign((size_t)L.MK.rows * L.MK.width, 0);
+        L.MK.val.assign((size_t)L.MK.rows * L.MK.width, 0.0);
+        L.MKk.assign((size_t)L.MK.rows * L.MK.width, 0.0);
+        std::vector<std::pair<int, std::pair<double, double>>> row;
+        for (int r = 0; r < m.n_edges; ++r) {
+            row.clear();
+            for (int s = 0; s < mk.cnt[r]; ++s)
+                row.push_back({mk.col[(size_t)r * cap + s], {mk.val[(size_t)r * cap + s], kk.val[(size_t)r * cap + s]}});
+            std::sort(row.begin(), row.end());
+            for (int s = 0; s < L.MK.width; ++s) {
+                const size_t o = (size_t)r * L.MK.width + s;
+                if (s < (int)row.size()) { L.MK.col[o] = row[s].first; L.MK.val[o] = row[s].second.first; L.MKk[o] = row[s].second.second; }
+                else L.MK.col[o] = r;
+            }
+        }
+    }
     L.dM = ell_diag(L.M);
     L.dK = ell_diag(L.K);
     L.dN = ell_diag(L.Kn);
