@@ -105,6 +105,23 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def ncu_traffic(family):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the finest-level launch of `family` from the
+    committed ncu --set full capture (profiles/r01_ncu_v3_kernels.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r01_ncu_v3_kernels.json")
+    if not os.path.exists(p):
+        return None
+    tag = {"residual": "k_residual", "sweep_update": "k_sweep", "gtr": "k_gtr"}.get(family)
+    with open(p) as fh:
+        for k in json.load(fh):
+            if tag and tag + "<" in k["Kernel Name"]:
+                def gb(s):
+                    v, u = s.split()[:2]
+                    return float(v) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(u, 1.0)
+                return gb(k["dram__bytes_read.sum"]) + gb(k["dram__bytes_write.sum"])
+    return None
+
+
 # ------------------------------------------------------------- CPU oracle
 def oracle_sample(n=32, S=8):
     """Bounded sample of the c4 workload for the CPU oracle: n^3 cells, S slabs, same lambda = 1."""
@@ -262,7 +279,7 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"time-slab blocks over {world} GPU(s) (NCCL halo/carry/norm collectives)"
                    if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": fam, "peak_source": peak_src,
+                     "traffic": ncu_traffic(fam), "kernel": fam, "peak_source": peak_src,
                      "kernel_share_of_step": kms / t_max,
                      "vcycle_algorithmic_GBps": total_bytes / (t_max * 1e-3) / 1e9},
         "gpu_launches": int(launches),
