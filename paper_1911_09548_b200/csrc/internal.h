@@ -130,7 +130,6 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
 void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, bool recon, const double *z,
                   const double *r, double *out, double omega_s, double omega);
 void launch_axpy(Stream st, size_t n, double alpha, const double *z, double *x);
-void launch_gt(Stream st, const DevLevel &L, int Q, const double *r, double omega_n, double *zn, double *w);
 void launch_gtr(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f, const double *prev,
                 double omega_n, double *zn, double *w);
 void launch_node_sweep(Stream st, const DevLevel &L, int Q, const double *z, const double *w, double omega_n,

@@ -423,47 +423,6 @@ __global__ void __launch_bounds__(kBlock) k_axpy(size_t n, double alpha, const d
 }
 
 // ------------------------------------------------------- nodal correction
-// w = G^T r at (node, k); zn = omega_n w / dN (first Jacobi sweep on K_n)
-template <int Q, int SPL, bool W_OUT>
-__global__ void __launch_bounds__(kBlock) k_gt(BoxMap m, DevELL GT, const double *__restrict__ r,
-                                               const double *__restrict__ dN, double omega_n,
-                                               double *__restrict__ zn, double *__restrict__ w) {
-    box_loop(m, [&](int node, int k0, bool valid) {
-    if (!valid) return;
-    const int S = m.S;
-    double acc[Q][SPL];
-#pragma unroll
-    for (int a = 0; a < Q; ++a)
-#pragma unroll
-        for (int j = 0; j < SPL; ++j) acc[a][j] = 0.0;
-    const int *c = GT.col + (size_t)node * GT.width;
-    for (int s = 0; s < GT.width; ++s) {
-        const int code = __ldg(c + s);
-        if (code < 0) break;
-        const double sg = (code & 1) ? -1.0 : 1.0;
-        const double *re = r + (size_t)(code >> 1) * Q * S + k0;
-#pragma unroll
-        for (int a = 0; a < Q; ++a) {
-            double v[SPL];
-            ldv<SPL>(re + a * S, v);
-#pragma unroll
-            for (int j = 0; j < SPL; ++j) acc[a][j] = fma(sg, v[j], acc[a][j]);
-        }
-    }
-    const double inv = omega_n / __ldg(dN + node);
-    const size_t base = (size_t)node * Q * S + k0;
-#pragma unroll
-    for (int a = 0; a < Q; ++a) {
-        double zv[SPL];
-#pragma unroll
-        for (int j = 0; j < SPL; ++j) zv[j] = acc[a][j] * inv;
-        stv<SPL>(zn + base + a * S, zv);
-        if (W_OUT) stv<SPL>(w + base + a * S, acc[a]);
-    }
-});
-}
-
-
 // Fused nodal residual (first half of Eq. 5): w = G^T (f - L x) computed per node without the
 // edge residual: G^T K = 0, so w = G^T f - sum_a Ct[b][a] (G^T M x_a) + e_0 (G^T M x_q)(k-1);
 // zn = omega_n w / d_n is the first Jacobi sweep on K_n (w stored for nu_n > 2).
@@ -1192,13 +1151,6 @@ void launch_axpy(Stream st, size_t n, double alpha, const double *z, double *x) 
     k_axpy<1><<<nblocks((long long)n), kBlock, 0, st>>>(n, alpha, z, x);
 }
 
-void launch_gt(Stream st, const DevLevel &L, int Q, const double *r, double omega_n, double *zn, double *w) {
-    const BoxMap m = node_map(L);
-    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, {
-        if (w) k_gt<QQ, SP, true><<<grid(m), kBlock, 0, st>>>(m, L.GT, r, L.dN, omega_n, zn, w);
-        else k_gt<QQ, SP, false><<<grid(m), kBlock, 0, st>>>(m, L.GT, r, L.dN, omega_n, zn, w);
-    }));
-}
 
 void launch_gtr(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f, const double *prev,
                 double omega_n, double *zn, double *w) {

@@ -37,44 +37,6 @@ __device__ __forceinline__ double cnu(const Grid3 &g, int i, int j, int k) {
     return cell_ok(g, i, j, k) ? __ldg(g.nu + i + g.nx * (j + g.ny * k)) : 0.0;
 }
 
-// Loop-invariant addressing of one pencil (j, k) for one lane: element offsets of the
-// stencil rows at x-position 0 (the row of x-position i is that + i), validity masks of
-// the transverse (j, k) neighbours, and the cell-plane offsets.
-struct Pencil {
-    int j, k;
-    int oX, oY, oZ;          // rows of X(0, j, k), Y(0, j, k), Z(0, j, k)
-    int sXj, sXk, sYj, sYk, sZj, sZk;   // row strides in j and k per direction
-    unsigned mX, mY, mZ;     // bit (dj+1)*3+(dk+1) (X), (dj+1)*3+(dk+1) (Y: dj<=0), (dj+1)*2+(dk+1) (Z: dk<=0)
-    int oC;                  // cell (0, j-1, k-1)
-    unsigned mC;             // bit dj*2+dk: cell (., j-1+dj, k-1+dk) exists in j/k
-};
-
-__device__ __forceinline__ Pencil make_pencil(const Grid3 &g, int j, int k) {
-    Pencil P;
-    P.j = j; P.k = k;
-    P.sXj = g.nx; P.sXk = g.nx * (g.ny + 1);
-    P.sYj = g.nx + 1; P.sYk = (g.nx + 1) * g.ny;
-    P.sZj = g.nx + 1; P.sZk = (g.nx + 1) * (g.ny + 1);
-    P.oX = j * P.sXj + k * P.sXk;
-    P.oY = g.Ex + j * P.sYj + k * P.sYk;
-    P.oZ = g.Ex + g.Ey + j * P.sZj + k * P.sZk;
-    P.mX = P.mY = P.mZ = P.mC = 0u;
-    for (int dj = -1; dj <= 1; ++dj)
-        for (int dk = -1; dk <= 1; ++dk) {
-            const int jj = j + dj, kk = k + dk;
-            if (jj >= 0 && jj <= g.ny && kk >= 0 && kk <= g.nz) P.mX |= 1u << ((dj + 1) * 3 + dk + 1);
-            if (dj <= 0 && jj >= 0 && jj < g.ny && kk >= 0 && kk <= g.nz) P.mY |= 1u << ((dj + 1) * 3 + dk + 1);
-            if (dk <= 0 && jj >= 0 && jj <= g.ny && kk >= 0 && kk < g.nz) P.mZ |= 1u << ((dj + 1) * 2 + dk + 1);
-        }
-    for (int dj = 0; dj < 2; ++dj)
-        for (int dk = 0; dk < 2; ++dk) {
-            const int jj = j - 1 + dj, kk = k - 1 + dk;
-            if (jj >= 0 && jj < g.ny && kk >= 0 && kk < g.nz) P.mC |= 1u << (dj * 2 + dk);
-        }
-    P.oC = (j - 1) * g.nx + (k - 1) * g.nx * g.ny;
-    return P;
-}
-
 // value loader for one lane: slab ks (ks < 0: the slab before the rank's first one)
 struct Lane {
     const double *x;
@@ -84,13 +46,6 @@ struct Lane {
         if (!ok) return 0.0;
         if (ks >= 0) return __ldg(x + (size_t)row * QS + a * S + ks);
         return (a == q && prev) ? __ldg(prev + row) : 0.0;
-    }
-    // branch-free stencil load: value of row `row` at base B with row stride RS, scaled by
-    // mult (0 for the halo lane when there is no previous-rank trace); !ok -> 0
-    __device__ __forceinline__ double ldo(const double *B, long long RS, double mult, int row, bool ok) const {
-        double v = 0.0;
-        if (ok) v = __ldg(B + row * RS);
-        return v * mult;
     }
 };
 
@@ -149,73 +104,6 @@ struct StepLoads {
     double Yn[2][3];   // Y(i+1, j+dj, k+dk), dj in {-1,0}
     double Zn[3][2];   // Z(i+1, j+dj, k+dk), dk in {-1,0}
 };
-
-struct LaneBase {
-    const double *B;   // x + a*S + ks, or the previous-rank trace (halo lane, time node q)
-    long long RS;      // row stride: Q*S, or 1 for the trace
-    double mult;       // 0 for the halo lane without a trace
-};
-
-__device__ __forceinline__ LaneBase lane_base(const double *x, const double *prev, int S, int Q, int a, int ks) {
-    LaneBase lb;
-    if (ks >= 0) { lb.B = x + (long long)a * S + ks; lb.RS = (long long)Q * S; lb.mult = 1.0; }
-    else if (prev && a == Q - 1) { lb.B = prev; lb.RS = 1; lb.mult = 1.0; }
-    else { lb.B = x; lb.RS = (long long)Q * S; lb.mult = 0.0; }
-    return lb;
-}
-
-__device__ __forceinline__ void load_step_p(const Grid3 &g, const Lane &ln, const Pencil &P, const LaneBase &lb,
-                                            int i, StepLoads &L) {
-    const bool xi = i < g.nx, yi = i + 1 <= g.nx;
-#pragma unroll
-    for (int dj = -1; dj <= 1; ++dj)
-#pragma unroll
-        for (int dk = -1; dk <= 1; ++dk)
-            L.Xc[dj + 1][dk + 1] = ln.ldo(lb.B, lb.RS, lb.mult, P.oX + i + dj * P.sXj + dk * P.sXk,
-                                          xi && ((P.mX >> ((dj + 1) * 3 + dk + 1)) & 1u));
-#pragma unroll
-    for (int dj = -1; dj <= 0; ++dj)
-#pragma unroll
-        for (int dk = -1; dk <= 1; ++dk)
-            L.Yn[dj + 1][dk + 1] = ln.ldo(lb.B, lb.RS, lb.mult, P.oY + i + 1 + dj * P.sYj + dk * P.sYk,
-                                          yi && ((P.mY >> ((dj + 1) * 3 + dk + 1)) & 1u));
-#pragma unroll
-    for (int dj = -1; dj <= 1; ++dj)
-#pragma unroll
-        for (int dk = -1; dk <= 0; ++dk)
-            L.Zn[dj + 1][dk + 1] = ln.ldo(lb.B, lb.RS, lb.mult, P.oZ + i + 1 + dj * P.sZj + dk * P.sZk,
-                                          yi && ((P.mZ >> ((dj + 1) * 2 + dk + 1)) & 1u));
-}
-
-// Y, Z at x-position 0 (window start)
-__device__ __forceinline__ void load_yz0(const Lane &ln, const Pencil &P, const LaneBase &lb,
-                                         double (&Yv)[2][3], double (&Zv)[3][2]) {
-#pragma unroll
-    for (int dj = -1; dj <= 0; ++dj)
-#pragma unroll
-        for (int dk = -1; dk <= 1; ++dk)
-            Yv[dj + 1][dk + 1] = ln.ldo(lb.B, lb.RS, lb.mult, P.oY + dj * P.sYj + dk * P.sYk, (P.mY >> ((dj + 1) * 3 + dk + 1)) & 1u);
-#pragma unroll
-    for (int dj = -1; dj <= 1; ++dj)
-#pragma unroll
-        for (int dk = -1; dk <= 0; ++dk)
-            Zv[dj + 1][dk + 1] = ln.ldo(lb.B, lb.RS, lb.mult, P.oZ + dj * P.sZj + dk * P.sZk, (P.mZ >> ((dj + 1) * 2 + dk + 1)) & 1u);
-}
-
-// cell plane at x-position i: cells (i, j-1+dj, k-1+dk)
-__device__ __forceinline__ void load_cell_plane(const Grid3 &g, const Pencil &P, int i, double (&s)[2][2],
-                                                double (&n)[2][2]) {
-    const bool ii = i < g.nx;
-#pragma unroll
-    for (int dj = 0; dj < 2; ++dj)
-#pragma unroll
-        for (int dk = 0; dk < 2; ++dk) {
-            const bool ok = ii && ((P.mC >> (dj * 2 + dk)) & 1u);
-            const int c = P.oC + i + dj * g.nx + dk * g.nx * g.ny;
-            s[dj][dk] = ok ? __ldg(g.sigma + c) : 0.0;
-            n[dj][dk] = ok ? __ldg(g.nu + c) : 0.0;
-        }
-}
 
 __device__ __forceinline__ void load_step(const Grid3 &g, const Lane &ln, int a, int i, int j, int k, StepLoads &L) {
     const bool xok_i = i < g.nx;
@@ -351,18 +239,6 @@ __device__ __forceinline__ void win_init(const Grid3 &g, const Lane &ln, int a, 
     w.Pyp = 0.0;
 }
 
-__device__ __forceinline__ void load_cells(const Grid3 &g, int i, int j, int k, Cells &c) {
-    // shift the i-1 plane in, load the cells at i
-#pragma unroll
-    for (int dj = 0; dj < 2; ++dj)
-#pragma unroll
-        for (int dk = 0; dk < 2; ++dk) {
-            c.s[0][dj][dk] = c.s[1][dj][dk];
-            c.n[0][dj][dk] = c.n[1][dj][dk];
-            c.s[1][dj][dk] = csig(g, i, j - 1 + dj, k - 1 + dk);
-            c.n[1][dj][dk] = cnu(g, i, j - 1 + dj, k - 1 + dk);
-        }
-}
 
 // all 8 cells around node (i, j, k) re-read each step (warp-broadcast L1 hits) instead of
 // carried in registers: the window then fits 168 registers without spills
