@@ -16,6 +16,7 @@
 // end value of slab k-1) and (Ct^{-1} e_0)_q = 1, checked in setup (R2).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <stdexcept>
 
 #include "internal.h"
@@ -107,7 +108,7 @@ __device__ __forceinline__ bool map_thread(const Map &m, int &row, int &k0) {
 // SPL slabs per lane.  Rows of one box share most of their ELL columns, so a
 // column's x chunk is fetched from L2 once per CTA and re-read from L1.
 struct BoxMap {
-    int S, spl, lpr_log2, rpw, chunk, n_boxes;
+    int S, spl, lpr_log2, rpw, chunk, n_boxes, n_chunks, box_major;
     const int *sched, *bptr;
 };
 
@@ -116,8 +117,9 @@ struct BoxMap {
 // row/slab, and must not store.
 template <class F>
 __device__ __forceinline__ void box_loop(const BoxMap &m, F &&body) {
-    const int chunk = blockIdx.x / m.n_boxes;
-    const int b = blockIdx.x - chunk * m.n_boxes;
+    int chunk, b;
+    if (m.box_major) { b = blockIdx.x / m.n_chunks; chunk = blockIdx.x - b * m.n_chunks; }
+    else { chunk = blockIdx.x / m.n_boxes; b = blockIdx.x - chunk * m.n_boxes; }
     const int beg = __ldg(m.bptr + b), end = __ldg(m.bptr + b + 1);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int k0 = chunk * m.chunk + (lane & ((1 << m.lpr_log2) - 1)) * m.spl;
@@ -1032,6 +1034,11 @@ static BoxMap make_boxmap(int S, const int *sched, const int *bptr, int n_boxes,
     m.rpw = 32 >> l2;
     m.chunk = (1 << l2) * m.spl;
     m.n_boxes = n_boxes;
+    m.n_chunks = (S + m.chunk - 1) / m.chunk;
+    // CTA order: all slab chunks of a box back to back (measured 2% faster than chunk-major);
+    // tuning knob ST_BOX_MAJOR=0 restores chunk-major
+    static const int order = [] { const char *e = std::getenv("ST_BOX_MAJOR"); return e ? std::atoi(e) : 1; }();
+    m.box_major = order;
     m.sched = sched;
     m.bptr = bptr;
     return m;

@@ -9,6 +9,8 @@
 // DESIGN.md §0(c).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -579,7 +581,11 @@ static double level_lambda(const HostLevel &L) {
 // start node; within a box: node order, then direction.
 static void box_schedule(const HostMesh &m, HostLevel &L) {
     const int d = m.dim;
-    const int B[3] = {d == 3 ? 4 : 8, d == 3 ? 2 : 4, d == 3 ? 2 : 1};
+    int B[3] = {d == 3 ? 4 : 8, d == 3 ? 2 : 4, d == 3 ? 2 : 1};
+    if (const char *e = std::getenv("ST_BOX")) {   // tuning knob: "bx,by,bz"
+        int a = 0, b = 0, c = 0;
+        if (std::sscanf(e, "%d,%d,%d", &a, &b, &c) == 3 && a > 0 && b > 0 && c > 0) { B[0] = a; B[1] = b; B[2] = d == 3 ? c : 1; }
+    }
     const int nn[3] = {m.n[0] + 1, m.n[1] + 1, d == 3 ? m.n[2] + 1 : 1};
     const int nb[3] = {(nn[0] + B[0] - 1) / B[0], (nn[1] + B[1] - 1) / B[1], (nn[2] + B[2] - 1) / B[2]};
     L.sched_e.clear(); L.bptr_e.assign(1, 0); L.sched_n.clear(); L.bptr_n.assign(1, 0);
