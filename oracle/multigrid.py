@@ -22,7 +22,9 @@ from .spacetime import Level, apply_L, hybrid_smooth, forward_solve
 class Options:
     spec: str = "SAS"
     omega: float = 0.5          # Eq. (2)
-    inner: str = "jacobi"       # 'jacobi' (GPU path definition) or 'exact'
+    inner: str = "jacobi"       # 'jacobi' (default GPU path), 'mg' (inner spatial V-cycle, R13) or 'exact'
+    nu_in: int = 2              # hybrid sweeps per side of the inner V-cycle (inner='mg')
+    omega_in: float = 0.4       # its edge damping: D^{-1}A reaches ~4 (2D) and dG(2) blocks need margin
     nu_s: int = 2               # block-Jacobi sweeps approximating A_k^{-1}
     omega_s: float = 0.6        # 3D default; 2D workloads use 0.5 (R3)
     nu_n: int = 2               # Jacobi sweeps approximating K_n^{-1}

@@ -12,6 +12,8 @@ PAPER.md references
 
 Inner spatial solves ("sufficiently well approximated", l.84):
   mode 'exact'   : A_k^{-1}, K_n^{-1} by sparse direct factorisation (LFA assumption, l.212)
+  mode 'mg'      : A_k^{-1} by one geometric V-cycle over the level's spatial chain with a
+                   hybrid edge / nodal smoother (R13; the role AMS plays in l.269)
   mode 'jacobi'  : the GPU hot path's fixed linear approximations (R3/R4):
                    nu_s damped block-Jacobi sweeps on A_k (one (q+1)x(q+1) block per edge),
                    nu_n damped Jacobi sweeps on K_n, both started from zero
@@ -97,12 +99,75 @@ def block_jacobi_inverse(lv, k, R, nu_s, omega_s):
     return z
 
 
+class SpatialChain:
+    """Spatial hierarchy of one level's mesh for the inner V-cycle (reading R13): the mesh and
+    its successive 2:1 coarsenings (coefficients averaged as for the outer hierarchy, R6)."""
+
+    def __init__(self, mesh, sigma, nu, q):
+        from . import fem
+        self.Ct, self.Mt, _ = time_dg.time_matrices(q)
+        self.Ctinv = np.linalg.inv(self.Ct)
+        self.lv = []
+        while True:
+            M, K, Kn = fem.assemble(mesh, sigma, nu)
+            G = fem.gradient(mesh).tocsr()
+            d = dict(M=M.tocsr(), K=K.tocsr(), G=G, GT=G.T.tocsr(), dM=M.diagonal(), dK=K.diagonal(),
+                     dN=Kn.diagonal(), n=mesh.n_edges, P=None)
+            self.lv.append(d)
+            if not mesh.can_coarsen():
+                break
+            mc = mesh.coarsen()
+            ch = mesh.child_cells()
+            d["P"] = fem.edge_prolongation(mesh, mc).tocsr()
+            sigma, nu, mesh = sigma[ch].mean(axis=1), nu[ch].mean(axis=1), mc
+
+    def A(self, j, tau, z):
+        L = self.lv[j]
+        return self.Ct @ (L["M"] @ z.T).T + tau * (self.Mt @ (L["K"] @ z.T).T)
+
+    def edge_sweep(self, j, tau, r, z, om):
+        """z + om D^{-1} (r - A z), D_e = Ct M_ee + tau Mt K_ee (R3)."""
+        L = self.lv[j]
+        D = self.Ct[None] * L["dM"][:, None, None] + tau * self.Mt[None] * L["dK"][:, None, None]
+        return z + om * np.einsum("eab,be->ae", np.linalg.inv(D), r - self.A(j, tau, z))
+
+    def nodal_step(self, j, tau, r, z, om):
+        """Hiptmair's nodal step on the gradient space: G^T A G = Ct (x) K_n (K G = 0), one
+        damped Jacobi sweep on it: z + G (om Ct^{-1} G^T (r - A z) / d_n)."""
+        L = self.lv[j]
+        w = (L["GT"] @ (r - self.A(j, tau, z)).T).T
+        y = om * (self.Ctinv @ w) / L["dN"][None, :]
+        return z + (L["G"] @ y.T).T
+
+    def vcycle(self, j, tau, r, opts):
+        """One V-cycle for A z = r (Q, n_j) from z = 0: nu_in hybrid sweeps (edge then nodal)
+        before, P^T / P to the next chain level, nu_in sweeps (nodal then edge) after; the
+        coarsest chain level only smooths."""
+        z = np.zeros_like(r)
+        for _ in range(opts.nu_in):
+            z = self.edge_sweep(j, tau, r, z, opts.omega_in)
+            z = self.nodal_step(j, tau, r, z, opts.omega_n)
+        P = self.lv[j]["P"]
+        if P is None:
+            return z
+        rc = (P.T @ (r - self.A(j, tau, z)).T).T
+        z = z + (P @ self.vcycle(j + 1, tau, rc, opts).T).T
+        for _ in range(opts.nu_in):
+            z = self.nodal_step(j, tau, r, z, opts.omega_n)
+            z = self.edge_sweep(j, tau, r, z, opts.omega_in)
+        return z
+
+
 def apply_B(lv, R, opts):
     """(I (x) A^{-1}) R with the configured inner approximation, slab by slab."""
     Z = np.zeros_like(R)
+    if opts.inner == "mg" and getattr(lv, "chain", None) is None:
+        lv.chain = SpatialChain(lv.mesh, lv.sigma, lv.nu, lv.q)
     for k in range(lv.S):
         if opts.inner == "exact":
             Z[k] = lv.Ainv_exact(k).solve(R[k].reshape(-1)).reshape(lv.q + 1, lv.n)
+        elif opts.inner == "mg":
+            Z[k] = lv.chain.vcycle(0, lv.tau[k], R[k], opts)
         else:
             Z[k] = block_jacobi_inverse(lv, k, R[k], opts.nu_s, opts.omega_s)
     return Z
