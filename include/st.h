@@ -76,6 +76,14 @@ typedef struct st_params {
                               With nranks > 1, tau is the GLOBAL slab array; this rank owns the
                               contiguous block [rank*n_slabs/nranks, (rank+1)*n_slabs/nranks)
                               and its vectors hold only that block (ST layout with S = block). */
+    /* approximation of A_k^{-1} inside S (Eq. 2; R13): inner = 0 (default) uses nu_s
+       damped block-Jacobi sweeps; inner = 1 one inner SPATIAL V-cycle per slab over the spatial
+       coarsening chain of the level's mesh, nu_in (default 2) hybrid sweeps per side: a damped
+       edge block-Jacobi sweep (omega_in, default 0.4) and a nodal step on range(G) (omega_n).
+       Pass 0 for the defaults. */
+    int inner;
+    int nu_in;
+    double omega_in;
 } st_params;
 
 typedef struct st_info_t {

@@ -30,7 +30,8 @@ class StParams(ctypes.Structure):
                 ("spec", ctypes.c_char_p), ("omega", ctypes.c_double), ("nu_s", ctypes.c_int),
                 ("omega_s", ctypes.c_double), ("nu_n", ctypes.c_int), ("omega_n", ctypes.c_double),
                 ("lambda_crit", ctypes.c_double), ("mode", ctypes.c_int), ("min_slabs", ctypes.c_int),
-                ("kernel_path", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int)]
+                ("kernel_path", ctypes.c_int), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
+                ("inner", ctypes.c_int), ("nu_in", ctypes.c_int), ("omega_in", ctypes.c_double)]
 
 
 class StInfo(ctypes.Structure):
@@ -114,7 +115,8 @@ def _dptr(a):
 
 
 def make_params(dim, n, sigma, nu, tau, q=1, coords=None, spec="SAS", omega=0.5, nu_s=2, omega_s=None,
-                nu_n=2, omega_n=0.6, lambda_crit=0.1, mode=0, min_slabs=1, kernel_path=0, rank=0, nranks=1):
+                nu_n=2, omega_n=0.6, lambda_crit=0.1, mode=0, min_slabs=1, kernel_path=0, rank=0, nranks=1,
+                inner="jacobi", nu_in=2, omega_in=0.4):
     """Fill an StParams; returns (params, keep-alive list)."""
     keep = [np.ascontiguousarray(sigma, dtype=np.float64), np.ascontiguousarray(nu, dtype=np.float64),
             np.ascontiguousarray(tau, dtype=np.float64), spec.encode()]
@@ -135,6 +137,9 @@ def make_params(dim, n, sigma, nu, tau, q=1, coords=None, spec="SAS", omega=0.5,
     p.lambda_crit, p.mode, p.min_slabs = lambda_crit, mode, min_slabs
     p.kernel_path = kernel_path
     p.rank, p.nranks = rank, nranks
+    if inner not in ("jacobi", "mg"):
+        raise ValueError("inner must be 'jacobi' or 'mg'")
+    p.inner, p.nu_in, p.omega_in = (1 if inner == "mg" else 0), nu_in, omega_in
     return p, keep
 
 
@@ -175,14 +180,15 @@ class Solver:
 
     def __init__(self, dim, n, sigma, nu, tau, q=1, coords=None, spec="SAS", omega=0.5, nu_s=2, omega_s=None,
                  nu_n=2, omega_n=0.6, lambda_crit=0.1, mode=0, min_slabs=1, kernel_path=0, rank=0, nranks=1,
-                 stream=None):
+                 inner="jacobi", nu_in=2, omega_in=0.4, stream=None):
         import torch
         if not torch.cuda.is_available():
             raise StError("no CUDA device: the space-time multigrid has no CPU path")
         lib = load()
         p, self._keep = make_params(dim, n, sigma, nu, tau, q=q, coords=coords, spec=spec, omega=omega, nu_s=nu_s,
                                     omega_s=omega_s, nu_n=nu_n, omega_n=omega_n, lambda_crit=lambda_crit, mode=mode,
-                                    min_slabs=min_slabs, kernel_path=kernel_path, rank=rank, nranks=nranks)
+                                    min_slabs=min_slabs, kernel_path=kernel_path, rank=rank, nranks=nranks,
+                                    inner=inner, nu_in=nu_in, omega_in=omega_in)
         self.dim, self.n, self.q = dim, tuple(n), q
         self.rank, self.nranks = rank, max(nranks, 1)
         self.S = p.n_slabs // self.nranks          # slabs of this rank's block

@@ -41,6 +41,7 @@ struct st_handle {
     std::vector<st::HostLevel> hl;
     std::vector<st::DevLevel> dl;   // this rank's levels 0..(g0 or L-1), local slab blocks
     std::vector<st::DevLevel> dg;   // rank 0 of a multi-rank run: global levels g0..L-1 ("gathered")
+    std::vector<std::vector<st::DevLevel>> inner;   // inner spatial V-cycle levels per smoothing level (R13)
     int rank = 0, nranks = 1, g0 = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -143,8 +144,66 @@ double nvec(const DevLevel &L, int Q) { return 8.0 * L.n_nodes * Q * L.S; }
 
 // prev: end values (time node q) of the slab before this level's first slab (the previous
 // rank's last slab), or null for the zero initial state (PAPER.md l.47-48 homogeneous u^0)
+// One inner spatial V-cycle (R13) for A_k z = r on all slabs at once (the slabs are
+// independent: no time coupling below the outer residual).  V[j] shares the chain operators
+// and its own vectors; returns the buffer holding z.  j = 0 enters with the first edge sweep
+// from zero already done (fused into the outer residual) and, with xout set, its last edge
+// sweep adds omega * z into xout instead of storing z.
+double *inner_vcycle(st_handle *h, std::vector<DevLevel> &V, int j, const double *r, double *xout) {
+    const auto &o = h->o;
+    auto s = (st::Stream)h->stream;
+    const int Q = h->Q;
+    DevLevel &I = V[j];
+    const double ev = evec(I, Q), nv = nvec(I, Q), ob = op_bytes(I);
+    const bool coarsest = j + 1 == (int)V.size();
+    double *cur = I.z, *oth = I.z2;
+    auto nodal = [&] {
+        h->run("in_nodal", 2 * ev + nv + ell_bytes(I.GtM) + 8.0 * I.n_nodes, 1,
+               [&] { st::launch_nodal_step(s, I, h->kt, Q, r, cur, o.omega_n, I.y); });
+        h->run("in_gupdate", 2 * ev + nv + 8.0 * I.n_edges, 1, [&] { st::launch_g_update(s, I, h->kt, Q, I.y, nullptr, cur); });
+    };
+    for (int i = 0; i < o.nu_in; ++i) {
+        if (i == 0) {
+            if (j > 0) h->run("in_jacobi", 2 * ev, 1, [&] { st::launch_jacobi_point(s, I, h->kt, Q, r, cur, o.omega_in); });
+        } else {
+            h->run("in_sweep", 3 * ev + ob, 1, [&] { st::launch_sweep(s, I, h->kt, Q, false, false, cur, r, oth, o.omega_in, 0.0); });
+            std::swap(cur, oth);
+        }
+        nodal();
+    }
+    if (coarsest) {
+        if (xout) h->run("axpy", 3 * ev, 1, [&] { st::launch_axpy(s, vec_len(I, Q), o.omega, cur, xout); });
+        return cur;
+    }
+    DevLevel &C = V[j + 1];
+    h->run("in_residual", 3 * ev + ob, 1, [&] { st::launch_residual_local(s, I, h->kt, Q, cur, r, oth); });
+    h->run("in_restrict", ev + evec(C, Q) + ell_bytes(I.Rg), 1, [&] { st::launch_space_transfer(s, I, C, Q, false, oth, C.r); });
+    double *zc = inner_vcycle(h, V, j + 1, C.r, nullptr);
+    h->run("in_prolong", 2 * ev + evec(C, Q) + ell_bytes(I.Pg), 1, [&] { st::launch_space_transfer(s, I, C, Q, true, zc, cur); });
+    for (int i = 0; i < o.nu_in; ++i) {
+        nodal();
+        if (xout && i + 1 == o.nu_in) {
+            h->run("in_sweep_update", 4 * ev + ob, 1, [&] { st::launch_sweep(s, I, h->kt, Q, true, false, cur, r, xout, o.omega_in, o.omega); });
+        } else {
+            h->run("in_sweep", 3 * ev + ob, 1, [&] { st::launch_sweep(s, I, h->kt, Q, false, false, cur, r, oth, o.omega_in, 0.0); });
+            std::swap(cur, oth);
+        }
+    }
+    return cur;
+}
+
 void smooth_S(st_handle *h, DevLevel &L, double *x, const double *f, const double *prev) {
     const auto &o = h->o;
+    if (o.inner == 1 && L.inner_id >= 0) {
+        // Eq. (2) with the inner V-cycle: r = f - L x and its first edge sweep z = omega_in D^{-1} r
+        // in one pass, then the rest of the inner cycle, whose last sweep performs x += omega z
+        auto &V = h->inner[L.inner_id];
+        h->run("residual", 4 * evec(L, h->Q) + op_bytes(L), 1, [&] {
+            st::launch_residual((st::Stream)h->stream, L, h->kt, h->Q, x, f, prev, V[0].r, V[0].z, o.omega_in, nullptr);
+        });
+        inner_vcycle(h, V, 0, V[0].r, x);
+        return;
+    }
     auto s = (st::Stream)h->stream;
     const int Q = h->Q;
     const double ev = evec(L, Q), ob = op_bytes(L);
@@ -319,6 +378,10 @@ static void parse_options(const st_params *p, st::Options &o) {
     if (p->nranks > 1 && (p->rank < 0 || p->rank >= p->nranks)) throw std::invalid_argument("rank out of range");
     if (p->nranks > 1 && p->n_slabs % p->nranks) throw std::invalid_argument("n_slabs must be a multiple of nranks");
     o.kernel_path = p->kernel_path;
+    if (p->inner < 0 || p->inner > 1) throw std::invalid_argument("inner must be 0 (block Jacobi) or 1 (spatial V-cycle)");
+    o.inner = p->inner;
+    if (p->nu_in > 0) o.nu_in = p->nu_in;
+    if (p->omega_in > 0) o.omega_in = p->omega_in;
 }
 
 const char *st_last_error(void) { return g_err.c_str(); }
@@ -410,6 +473,59 @@ int st_setup(const st_params *p, st_handle **out) {
         }
         if (P > 1 && h->rank == 0)
             for (int l = h->g0; l < L; ++l) h->dg.push_back(build(l, 0, (int)h->hl[l].tau.size(), l == L - 1, true));
+        if (o.inner == 1) {
+            // inner spatial V-cycle (R13): the chain operators are uploaded once and shared by
+            // every smoothing level; each level gets its own vectors on its chain segment
+            std::vector<st::HostLevel> chain;
+            st::build_chain(h->hl[0], chain);
+            std::vector<DevLevel> ops;
+            for (auto &C : chain) {
+                DevLevel D;
+                D.n_edges = C.mesh.n_edges; D.n_nodes = C.mesh.n_nodes; D.Q = Q;
+                D.M = h->upload(C.M); D.K = h->upload(C.K); D.GT = h->upload(C.GT); D.GtM = h->upload(C.GtM);
+                std::vector<double2> mkv(C.MK.val.size());
+                for (size_t i = 0; i < mkv.size(); ++i) mkv[i] = make_double2(C.MK.val[i], C.MKk[i]);
+                D.mk_width = C.MK.width; D.mk_col = h->upload(C.MK.col); D.mk_val = h->upload(mkv);
+                D.dM = h->upload(C.dM); D.dK = h->upload(C.dK); D.dN = h->upload(C.dN);
+                D.edge_nodes = h->upload(C.mesh.edge_nodes);
+                D.sched_e = h->upload(C.sched_e); D.bptr_e = h->upload(C.bptr_e);
+                D.sched_n = h->upload(C.sched_n); D.bptr_n = h->upload(C.bptr_n);
+                D.nbox_e = (int)C.bptr_e.size() - 1; D.nbox_n = (int)C.bptr_n.size() - 1;
+                if (C.space_coarsened) { D.Pg = h->upload(C.Pg); D.Rg = h->upload(C.Rg); }
+                if (const char *e = std::getenv("ST_EDGE_LPR")) D.lpr_log2 = std::max(0, std::min(5, std::atoi(e)));
+                ops.push_back(D);
+            }
+            auto attach = [&](std::vector<DevLevel> &levels, int l0) {
+                for (size_t i = 0; i < levels.size(); ++i) {
+                    DevLevel &D = levels[i];
+                    const int l = l0 + (int)i;
+                    if (D.Ainv) continue;   // the coarsest level solves exactly
+                    int ci = 0;
+                    for (int k = 0; k < l; ++k) ci += h->hl[k].space_coarsened ? 1 : 0;
+                    std::vector<DevLevel> V;
+                    for (int c = ci; c < (int)ops.size(); ++c) {
+                        DevLevel I = ops[c];
+                        I.S = D.S; I.tau = D.tau;
+                        const size_t ve = vec_len(I, Q), vn = vec_len(I, Q, true);
+                        if (c == ci) {
+                            I.r = D.r;
+                            I.z = h->dalloc<double>(ve);
+                        } else {
+                            I.r = h->dalloc<double>(ve);
+                            I.z = h->dalloc<double>(ve);
+                        }
+                        I.z2 = h->dalloc<double>(ve);
+                        I.y = h->dalloc<double>(vn);
+                        V.push_back(I);
+                    }
+                    if (ops[ci].n_edges != D.n_edges) throw std::logic_error("spatial chain does not match the level mesh");
+                    D.inner_id = (int)h->inner.size();
+                    h->inner.push_back(std::move(V));
+                }
+            };
+            attach(h->dl, 0);
+            attach(h->dg, h->g0);
+        }
         for (st::HostLevel &H : h->hl) {   // the device owns the operators now; keep the metadata
             H.M = H.K = H.Kn = H.GT = H.Pg = H.Rg = H.GtM = H.MK = st::HostELL();
             std::vector<double>().swap(H.MKk);

@@ -98,6 +98,7 @@ struct DevLevel {
     double *Pt = nullptr;
     double *Ainv = nullptr;
     bool space_coarsened = false;
+    int inner_id = -1;      // index of this level's inner spatial V-cycle levels (st_handle::inner), -1: none
     // work vectors (ST layout)
     double *x = nullptr, *f = nullptr;          // coarse levels only (level 0 uses caller's)
     double *r = nullptr, *z = nullptr, *z2 = nullptr;    // edge temporaries
@@ -114,6 +115,9 @@ struct Options {
     double lambda_crit = 0.1;
     int mode = 0;
     int min_slabs = 1;
+    int inner = 0;          // 0: nu_s block-Jacobi sweeps for A_k^{-1}; 1: inner spatial V-cycle (R13)
+    int nu_in = 2;
+    double omega_in = 0.4;
     int kernel_path = 0;    // 0: assembled ELL operators (default); 1: matrix-free pencil march on uniform hex levels
 };
 
@@ -143,6 +147,13 @@ void launch_end_values(Stream st, int rows, int Q, int S, const double *x, doubl
 void launch_restrict(Stream st, const DevLevel &F, const DevLevel &C, int Q, const double *r, double *fc);
 void launch_prolong(Stream st, const DevLevel &F, int Q, const double *xc, double *x);
 int launch_coarsest(Stream st, const DevLevel &L, int Q, const double *f, double *x);
+void launch_residual_local(Stream st, const DevLevel &L, const KT &kt, int Q, const double *z, const double *r,
+                           double *d);
+void launch_nodal_step(Stream st, const DevLevel &L, const KT &kt, int Q, const double *r, const double *z,
+                       double omega_n, double *y);
+void launch_jacobi_point(Stream st, const DevLevel &L, const KT &kt, int Q, const double *r, double *z, double omega);
+void launch_space_transfer(Stream st, const DevLevel &F, const DevLevel &C, int Q, bool prolong, const double *in,
+                           double *out);
 void launch_reduce(Stream st, int n, const double *partial, double *out);
 int launch_norm2(Stream st, size_t n, const double *v, double *partial);
 int residual_partials(const DevLevel &L);
@@ -151,6 +162,7 @@ int residual_partials(const DevLevel &L);
 TimeMats time_matrices(int q);
 HostMesh make_mesh(int dim, const int n[3], const double *coords);
 void assemble(HostLevel &L);
+void build_chain(const HostLevel &L0, std::vector<HostLevel> &chain);
 void build_hierarchy(const st_params &p, const Options &o, const TimeMats &tm,
                      std::vector<HostLevel> &levels);
 

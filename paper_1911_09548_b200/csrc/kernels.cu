@@ -292,7 +292,7 @@ __device__ __forceinline__ void coupling(const DevELL &M, int row, int k0, int S
 // ------------------------------------------------------------ residual
 // r = f - L x; optionally z = omega_s D^{-1} r (first Jacobi sweep of B from zero)
 // and per-block partial sums of |r|^2.
-template <int Q, int SPL, int WM, int WK, bool R_OUT, bool Z_OUT, bool NORM>
+template <int Q, int SPL, int WM, int WK, bool R_OUT, bool Z_OUT, bool NORM, bool COUPLE = true>
 __global__ void __launch_bounds__(kBlock) k_residual(BoxMap m, DevELL M, MKELL MK, const double *__restrict__ tau,
                                                      const double *__restrict__ x, const double *__restrict__ f,
                                                      const double *__restrict__ prev, double *__restrict__ r,
@@ -304,7 +304,10 @@ __global__ void __launch_bounds__(kBlock) k_residual(BoxMap m, DevELL M, MKELL M
         const int S = m.S;
         double mx[Q][SPL], kx[Q][SPL], mp[SPL];
         spatial_apply_mk<Q, SPL, WK>(MK, row, k0, S, x, mx, kx);
-        coupling<Q, SPL, WM>(M, row, k0, S, 1 << m.lpr_log2, x, prev, mx, mp);
+        if (COUPLE) coupling<Q, SPL, WM>(M, row, k0, S, 1 << m.lpr_log2, x, prev, mx, mp);
+        else
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) mp[j] = 0.0;
         if (!valid) return;
         double t[SPL];
         ldv<SPL>(tau + k0, t);
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(kBlock) k_axpy(size_t n, double alpha, const d
 // Fused nodal residual (first half of Eq. 5): w = G^T (f - L x) computed per node without the
 // edge residual: G^T K = 0, so w = G^T f - sum_a Ct[b][a] (G^T M x_a) + e_0 (G^T M x_q)(k-1);
 // zn = omega_n w / d_n is the first Jacobi sweep on K_n (w stored for nu_n > 2).
-template <int Q, int SPL, bool W_OUT>
+template <int Q, int SPL, bool W_OUT, bool COUPLE = true, bool CTINV = false>
 __global__ void __launch_bounds__(kBlock) k_gtr(BoxMap m, DevELL GT, DevELL GtM, const double *__restrict__ x,
                                                 const double *__restrict__ f, const double *__restrict__ prev,
                                                 const double *__restrict__ dN, double omega_n, KT kt,
@@ -459,9 +462,11 @@ __global__ void __launch_bounds__(kBlock) k_gtr(BoxMap m, DevELL GT, DevELL GtM,
         const int lpr = 1 << m.lpr_log2;
         double mp[SPL];
 #pragma unroll
-        for (int j = 1; j < SPL; ++j) mp[j] = gm[Q - 1][j - 1];
+        for (int j = 1; j < SPL; ++j) mp[j] = COUPLE ? gm[Q - 1][j - 1] : 0.0;
         const double up = __shfl_up_sync(0xffffffffu, gm[Q - 1][SPL - 1], 1, lpr);
-        if (((threadIdx.x & 31) & (lpr - 1)) != 0) {
+        if (!COUPLE) {
+            mp[0] = 0.0;
+        } else if (((threadIdx.x & 31) & (lpr - 1)) != 0) {
             mp[0] = up;
         } else {
             double acc = 0.0;
@@ -495,19 +500,31 @@ __global__ void __launch_bounds__(kBlock) k_gtr(BoxMap m, DevELL GT, DevELL GtM,
         }
         const double inv = omega_n / __ldg(dN + node);
         const size_t base = (size_t)node * QS + k0;
+        double wv[Q][SPL];
 #pragma unroll
-        for (int b = 0; b < Q; ++b) {
-            double wv[SPL], zv[SPL];
+        for (int b = 0; b < Q; ++b)
 #pragma unroll
             for (int j = 0; j < SPL; ++j) {
                 double acc = 0.0;
 #pragma unroll
                 for (int a = 0; a < Q; ++a) acc += kt.Ct[b * Q + a] * gm[a][j];
-                wv[j] = gf[b][j] - acc + (b == 0 ? mp[j] : 0.0);
-                zv[j] = wv[j] * inv;
+                wv[b][j] = gf[b][j] - acc + (b == 0 ? mp[j] : 0.0);
+            }
+#pragma unroll
+        for (int b = 0; b < Q; ++b) {
+            double zv[SPL];
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) {
+                double v = wv[b][j];
+                if (CTINV) {   // inner hybrid smoother: y = omega_n Ct^{-1} w / d_n (R13)
+                    v = 0.0;
+#pragma unroll
+                    for (int a = 0; a < Q; ++a) v += kt.Ctinv[b * Q + a] * wv[a][j];
+                }
+                zv[j] = v * inv;
             }
             stv<SPL>(zn + base + b * S, zv);
-            if (W_OUT) stv<SPL>(w + base + b * S, wv);
+            if (W_OUT) stv<SPL>(w + base + b * S, wv[b]);
         }
     });
 }
@@ -876,6 +893,49 @@ __global__ void __launch_bounds__(32 * kMarchWarps, 3) k_sweep_march(MarchMap mm
 // ------------------------------------------------------------- transfers
 // Restriction: fc[rc][a][K] = sum_{(rf,w) in R_s row rc} w * sum_{j,b} Pt_K[(j Q + b)][a] r[rf][b][2K+j]
 // one thread per (coarse row, coarse slab K); the fine slab pair (2K, 2K+1) is one 16-byte load.
+// space-only restriction / prolongation of the inner spatial V-cycle (R13): same slabs
+template <int Q, bool PROLONG>
+__global__ void __launch_bounds__(kBlock) k_space_transfer(Map m, DevELL T, const double *__restrict__ in,
+                                                           double *__restrict__ out) {
+    int row, k;
+    if (!map_thread(m, row, k)) return;
+    const int S = m.S;
+    double acc[Q];
+#pragma unroll
+    for (int a = 0; a < Q; ++a) acc[a] = 0.0;
+    for (int s = 0; s < T.width; ++s) {
+        double wgt; int c;
+        ld_ent(T.e + (size_t)row * T.width + s, wgt, c);
+        const double *src = in + (size_t)c * Q * S + k;
+#pragma unroll
+        for (int a = 0; a < Q; ++a) acc[a] = fma(wgt, __ldg(src + a * S), acc[a]);
+    }
+    const size_t base = (size_t)row * Q * S + k;
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+        if (PROLONG) out[base + a * S] += acc[a];
+        else out[base + a * S] = acc[a];
+    }
+}
+
+// z = omega D^{-1} r (the first block-Jacobi sweep from zero), pointwise
+template <int Q>
+__global__ void __launch_bounds__(kBlock) k_jacobi_point(Map m, const double *__restrict__ tau,
+                                                         const double *__restrict__ dM, const double *__restrict__ dK,
+                                                         const double *__restrict__ r, double *__restrict__ z,
+                                                         double omega, KT kt) {
+    int row, k;
+    if (!map_thread(m, row, k)) return;
+    const int S = m.S;
+    const size_t base = (size_t)row * Q * S + k;
+    double v[Q], y[Q];
+#pragma unroll
+    for (int a = 0; a < Q; ++a) v[a] = __ldg(r + base + a * S);
+    block_solve<Q>(kt, __ldg(dM + row), __ldg(dK + row), __ldg(tau + k), v, y);
+#pragma unroll
+    for (int a = 0; a < Q; ++a) z[base + a * S] = omega * y[a];
+}
+
 template <int Q, bool SPACE>
 __global__ void __launch_bounds__(kBlock) k_restrict(Map m, DevELL Rg, const double *__restrict__ r,
                                                      const double *__restrict__ Pt, double *__restrict__ fc) {
@@ -1213,6 +1273,38 @@ void launch_prolong(Stream st, const DevLevel &F, int Q, const double *xc, doubl
     ST_DISPATCH_Q(Q, {
         if (F.space_coarsened) k_prolong<QQ, true><<<grid(m), kBlock, 0, st>>>(m, F.Pg, xc, F.Pt, x);
         else k_prolong<QQ, false><<<grid(m), kBlock, 0, st>>>(m, F.Pg, xc, F.Pt, x);
+    });
+}
+
+// inner spatial V-cycle pieces (R13)
+void launch_residual_local(Stream st, const DevLevel &L, const KT &kt, int Q, const double *z, const double *r,
+                           double *d) {
+    const BoxMap m = edge_map(L);
+    const MKELL MK{L.mk_col, L.mk_val, L.mk_width};
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.mk_width, {
+        k_residual<QQ, SP, WM_, WK_, true, false, false, false><<<grid(m), kBlock, 0, st>>>(m, L.M, MK, L.tau, z, r, nullptr, d, nullptr, L.dM, L.dK, 0.0, kt, nullptr);
+    })));
+}
+
+void launch_nodal_step(Stream st, const DevLevel &L, const KT &kt, int Q, const double *r, const double *z,
+                       double omega_n, double *y) {
+    const BoxMap m = make_boxmap(L.S, L.sched_n, L.bptr_n, L.nbox_n, L.lpr_log2);
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, {
+        k_gtr<QQ, SP, false, false, true><<<grid(m), kBlock, 0, st>>>(m, L.GT, L.GtM, z, r, nullptr, L.dN, omega_n, kt, y, nullptr);
+    }));
+}
+
+void launch_jacobi_point(Stream st, const DevLevel &L, const KT &kt, int Q, const double *r, double *z, double omega) {
+    const Map m = make_map(L.n_edges, L.S, false);
+    ST_DISPATCH_Q(Q, k_jacobi_point<QQ><<<grid(m), kBlock, 0, st>>>(m, L.tau, L.dM, L.dK, r, z, omega, kt));
+}
+
+void launch_space_transfer(Stream st, const DevLevel &F, const DevLevel &C, int Q, bool prolong, const double *in,
+                           double *out) {
+    const Map m = make_map(prolong ? F.n_edges : C.n_edges, F.S, false);
+    ST_DISPATCH_Q(Q, {
+        if (prolong) k_space_transfer<QQ, true><<<grid(m), kBlock, 0, st>>>(m, F.Pg, in, out);
+        else k_space_transfer<QQ, false><<<grid(m), kBlock, 0, st>>>(m, F.Rg, in, out);
     });
 }
 

@@ -630,6 +630,30 @@ static void detect_uniform(HostLevel &L) {
     for (int a = 0; a < 3; ++a) L.hbox[a] = h[a];
 }
 
+// Spatial coarsening chain of the finest mesh for the inner V-cycle (R13): chain[i] is the
+// mesh coarsened i times (coefficients averaged as for the outer hierarchy, R6), with the
+// transfers chain[i] -> chain[i+1] in chain[i].Pg / Rg.  Every outer level's mesh is one of
+// them (outer level l sits at chain index = number of space coarsenings above it).
+void build_chain(const HostLevel &L0, std::vector<HostLevel> &chain) {
+    chain.clear();
+    chain.emplace_back();
+    chain[0].mesh = L0.mesh; chain[0].sigma = L0.sigma; chain[0].nu = L0.nu; chain[0].ratio_min = L0.ratio_min;
+    for (size_t i = 0;; ++i) {
+        HostLevel &C = chain[i];
+        assemble(C);
+        box_schedule(C.mesh, C);
+        const HostMesh &m = C.mesh;
+        bool can = true;
+        for (int a = 0; a < m.dim; ++a) can = can && (m.n[a] % 2 == 0) && m.n[a] >= 2;
+        if (!can) break;
+        HostLevel N;
+        coarsen_mesh(C, N);
+        build_transfers(C.mesh, N.mesh, C.Pg, C.Rg);
+        C.space_coarsened = true;
+        chain.push_back(std::move(N));
+    }
+}
+
 void build_hierarchy(const st_params &p, const Options &o, const TimeMats &tm, std::vector<HostLevel> &levels) {
     const int Q = tm.Q, q = Q - 1;
     levels.clear();
