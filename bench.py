@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-out", default=None, help="write per-kernel event stats (json)")
     ap.add_argument("--kernel-path", type=int, default=0, help="0: assembled ELL (default), 1: matrix-free march")
+    ap.add_argument("--inner", default="jacobi", choices=["jacobi", "mg"],
+                    help="A_k^{-1} inside S: block-Jacobi sweeps (default) or the inner spatial V-cycle (R13)")
     return ap.parse_args()
 
 
@@ -47,7 +49,8 @@ def workload(args):
 
 def workload_name(args):
     return (f"c4: unit cube {args.n}^3 hex, lowest-order Nedelec, dG(1), tau=1/4096, sigma=nu=1, "
-            f"{args.slabs} slabs per GPU, f ~ U(-1,1) seed 3")
+            f"{args.slabs} slabs per GPU, f ~ U(-1,1) seed 3"
+            + ("" if args.inner == "jacobi" else ", inner spatial V-cycle for A_k^{-1} (R13)"))
 
 
 # ------------------------------------------------------------------ clocks
@@ -186,7 +189,8 @@ def run_ours(args, rank, world, local_rank):
     w = workloads.c4(n=args.n, S=args.slabs * world, tau=1.0 / 4096)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        s = p.Solver.from_workload(w, stream=stream, rank=rank, nranks=world, kernel_path=args.kernel_path)
+        s = p.Solver.from_workload(w, stream=stream, rank=rank, nranks=world, kernel_path=args.kernel_path,
+                                   inner=args.inner)
         g = torch.Generator(device="cuda")
         g.manual_seed(3 + 1000 * rank)
         f = torch.empty(s.shape, dtype=torch.float64, device="cuda").uniform_(-1.0, 1.0, generator=g)

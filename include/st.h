@@ -115,6 +115,13 @@ int st_residual(st_handle *h, const double *x, const double *f, double *r, doubl
  * Asynchronous on the handle's stream. */
 int st_vcycle(st_handle *h, double *x, const double *f);
 
+/* enable = 1: st_vcycle and st_solve replay the V-cycle's launch sequence as a CUDA graph,
+ * captured on first use for each (x, f) pointer pair (the graph bakes the pointers in; at most
+ * 8 pairs are kept, oldest evicted).  Removes the host launch cost of the ~10^2-10^3 kernels of
+ * a cycle (small problems are launch-bound).  Ignored while st_profile is recording.
+ * enable = 0 (default) launches kernels directly and frees the graphs. */
+int st_set_graphs(st_handle *h, int enable);
+
 /* V-cycles from the given x until ||f - L x|| <= tol ||f|| or maxit cycles.
  * Device pointers.  *iters (host) = cycles run; hist (host, maxit+1 doubles,
  * may be NULL) = relative residual before each cycle and after the last. */

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libst.so")
 LEVEL_OPS = ["st_lv_count", "st_lv_get", "st_lv_residual", "st_lv_smooth_S", "st_lv_correct_local",
              "st_lv_correct_apply", "st_lv_restrict", "st_lv_prolong", "st_lv_vcycle", "st_lv_end_values",
              "st_copy_slabs", "st_zero", "st_sync"]
-EXPORTED = ["st_setup", "st_free", "st_set_stream", "st_residual", "st_vcycle", "st_solve",
+EXPORTED = ["st_setup", "st_free", "st_set_stream", "st_residual", "st_vcycle", "st_set_graphs", "st_solve",
             "st_solve_host", "st_info", "st_profile", "st_profile_read", "st_plan", "st_host_matrix",
             *LEVEL_OPS, "st_last_error"]
 
@@ -72,6 +72,7 @@ def load():
     lib.st_set_stream.argtypes = [vp, vp]
     lib.st_residual.argtypes = [vp, vp, vp, vp, dp]
     lib.st_vcycle.argtypes = [vp, vp, vp]
+    lib.st_set_graphs.argtypes = [vp, ctypes.c_int]
     lib.st_solve.argtypes = [vp, vp, vp, ctypes.c_double, ctypes.c_int, ip, dp]
     lib.st_solve_host.argtypes = [vp, dp, dp, ctypes.c_double, ctypes.c_int, ip, dp]
     lib.st_info.argtypes = [vp, ctypes.POINTER(StInfo)]
@@ -237,6 +238,10 @@ class Solver:
 
     def vcycle(self, x, f):
         _check(load().st_vcycle(self._h, self._chk(x), self._chk(f)))
+
+    def set_graphs(self, enable=True):
+        """Replay the V-cycle as a captured CUDA graph per (x, f) pair (st_set_graphs)."""
+        _check(load().st_set_graphs(self._h, 1 if enable else 0))
 
     def solve(self, x, f, tol=1e-8, maxit=100):
         it = ctypes.c_int()

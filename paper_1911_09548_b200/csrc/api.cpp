@@ -53,6 +53,15 @@ struct st_handle {
     int64_t bytes = 0;
     std::vector<void *> allocs;
     int64_t n_dofs = 0;
+    // CUDA-graph replay of the single-process V-cycle (st_set_graphs)
+    bool use_graphs = false;
+    cudaStream_t cap_stream = nullptr;
+    struct Graph { const double *x, *f; cudaGraphExec_t exec; int64_t launches; };
+    std::vector<Graph> graphs;
+    void clear_graphs() {
+        for (auto &g : graphs) cudaGraphExecDestroy(g.exec);
+        graphs.clear();
+    }
     // profiling: (family, bytes, start, stop) per recorded launch
     bool prof = false;
     struct Rec { int fam; double bytes; cudaEvent_t a, b; };
@@ -122,6 +131,8 @@ struct st_handle {
         return d;
     }
     ~st_handle() {
+        clear_graphs();
+        if (cap_stream) cudaStreamDestroy(cap_stream);
         for (auto &r : recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
         for (auto e : pool) cudaEventDestroy(e);
         for (void *p : allocs) cudaFree(p);
@@ -297,6 +308,49 @@ void vcycle(st_handle *h, std::vector<DevLevel> &V, int l, double *x, const doub
     vcycle(h, V, l + 1, C.x, C.f);
     prolong_from(h, L, C, C.x, x);
     hybrid(h, L, x, f, false);
+}
+
+// the single-process V-cycle on the finest level, through a captured CUDA graph when enabled
+void run_vcycle(st_handle *h, double *x, const double *f) {
+    if (!h->use_graphs || h->prof || h->debug_sync) { vcycle(h, h->dl, 0, x, f); return; }
+    for (auto &g : h->graphs)
+        if (g.x == x && g.f == f) {
+            ck(cudaGraphLaunch(g.exec, h->stream), "graph launch");
+            h->launches += g.launches;
+            return;
+        }
+    if (h->graphs.size() >= 8) {
+        cudaGraphExecDestroy(h->graphs.front().exec);
+        h->graphs.erase(h->graphs.begin());
+    }
+    // capture on a private stream (the user's may be the legacy default stream, which cannot
+    // capture); nothing executes during capture, the graph is launched on the user's stream
+    if (!h->cap_stream) ck(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking), "capture stream");
+    const int64_t l0 = h->launches;
+    cudaGraph_t graph = nullptr;
+    cudaStream_t user = h->stream;
+    h->stream = h->cap_stream;
+    ck(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+        vcycle(h, h->dl, 0, x, f);
+    } catch (...) {
+        cudaStreamEndCapture(h->stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        h->stream = user;
+        h->launches = l0;
+        throw;
+    }
+    cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+    h->stream = user;
+    ck(ce, "end capture");
+    st_handle::Graph g{x, f, nullptr, h->launches - l0};
+    h->launches = l0;
+    cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    ck(e, "graph instantiate");
+    h->graphs.push_back(g);
+    ck(cudaGraphLaunch(g.exec, h->stream), "graph launch");
+    h->launches += g.launches;
 }
 
 // ||f - L x||^2 (f != null) on level 0 without storing r
@@ -591,7 +645,17 @@ int st_residual(st_handle *h, const double *x, const double *f, double *r, doubl
 int st_vcycle(st_handle *h, double *x, const double *f) {
     if (!h || !x || !f) return fail(1, "null argument");
     if (h->nranks > 1) return fail(1, "multi-rank handles run the V-cycle through the st_lv_* level operations");
-    ST_GUARD(vcycle(h, h->dl, 0, x, f))
+    ST_GUARD(run_vcycle(h, x, f))
+}
+
+int st_set_graphs(st_handle *h, int enable) {
+    if (!h) return fail(1, "null handle");
+    if (enable && h->nranks > 1) return fail(1, "graphs apply to the single-process V-cycle only");
+    ST_GUARD({
+        ck(cudaStreamSynchronize(h->stream), "sync");
+        h->clear_graphs();
+        h->use_graphs = enable != 0;
+    })
 }
 
 int st_solve(st_handle *h, double *x, const double *f, double tol, int maxit, int *iters, double *hist) {
@@ -604,7 +668,7 @@ int st_solve(st_handle *h, double *x, const double *f, double tol, int maxit, in
             const double rel = std::sqrt(residual_norm2(h, x, f)) / nf;
             if (hist) hist[it] = rel;
             if (rel <= tol || it == maxit) break;
-            vcycle(h, h->dl, 0, x, f);
+            run_vcycle(h, x, f);
         }
         if (iters) *iters = it;
     })

@@ -88,6 +88,7 @@ def reference(name, q, opts, maxit):
     (2, "c5", 1, {}),              # jittered mesh, geometric tau (non-uniform split points)
     (2, "c1", 1, {"min_slabs": 4}),   # the coarsest level itself is distributed
     (2, "c2", 1, {"spec": "ASA", "nu_s": 1, "nu_n": 3}),
+    (2, "c1", 1, {"inner": "mg"}),    # inner spatial V-cycle (R13) on the local slab blocks
 ])
 def test_distributed_vcycle_matches_single_process(P, name, q, opts):
     Xd, _, g0 = run(P, name, q, opts)

@@ -50,7 +50,7 @@ def test_driver_single_rank_bitwise(name):
     assert torch.equal(xa, xb)
 
 
-def _worker(rank, P, port, name, out):
+def _worker(rank, P, port, name, out, opts=None):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -61,7 +61,7 @@ def _worker(rank, P, port, name, out):
         torch.cuda.set_device(0)
         w = workloads.small(name)
         X0, F = _inputs(w)
-        s = p.Solver.from_workload(w, rank=rank, nranks=P)
+        s = p.Solver.from_workload(w, rank=rank, nranks=P, **(opts or {}))
         cnt = w.S // P
         x = torch.from_numpy(np.ascontiguousarray(X0[:, :, rank * cnt:(rank + 1) * cnt])).cuda()
         f = torch.from_numpy(np.ascontiguousarray(F[:, :, rank * cnt:(rank + 1) * cnt])).cuda()
@@ -77,8 +77,9 @@ def _worker(rank, P, port, name, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,P", [("c1", 2), ("c4", 2), ("c5", 2), ("c1", 4)])
-def test_two_ranks_one_gpu(name, P):
+@pytest.mark.parametrize("name,P,opts", [("c1", 2, {}), ("c4", 2, {}), ("c5", 2, {}), ("c1", 4, {}),
+                                         ("c4", 2, {"inner": "mg"})])
+def test_two_ranks_one_gpu(name, P, opts):
     import torch.multiprocessing as mp
     import paper_1911_09548_b200 as p
     from paper_1911_09548_b200 import build as _b
@@ -86,7 +87,7 @@ def test_two_ranks_one_gpu(name, P):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, P, port, name, q)) for r in range(P)]
+    procs = [ctx.Process(target=_worker, args=(r, P, port, name, q, opts)) for r in range(P)]
     for pr in procs:
         pr.start()
     Xd, hist = q.get(timeout=600)
@@ -95,7 +96,7 @@ def test_two_ranks_one_gpu(name, P):
         assert pr.exitcode == 0
     w = workloads.small(name)
     X0, F = _inputs(w)
-    s = p.Solver.from_workload(w)
+    s = p.Solver.from_workload(w, **opts)
     x = torch.from_numpy(X0).cuda()
     f = torch.from_numpy(F).cuda()
     s.vcycle(x, f)

@@ -80,3 +80,24 @@ def test_fullsize_vcycle_contracts(torch_cuda, name):
     x0 = torch.zeros_like(f)
     s.vcycle(x0, z)
     assert torch.count_nonzero(x0).item() == 0
+
+
+def test_fullsize_c5_converges(torch_cuda):
+    # BASELINE c5 at full size (48^3 jittered, 2048 geometric slabs, contrast 1e5): the workload's
+    # omega_s keeps the block-Jacobi smoother contracting, and the inner spatial V-cycle (R13)
+    # converges several times faster per cycle
+    torch = torch_cuda
+    import paper_1911_09548_b200 as p
+    w = workloads.c5()
+    f = w.rhs_device()
+    rates = {}
+    for inner in ("jacobi", "mg"):
+        s = p.Solver.from_workload(w, inner=inner)
+        x = torch.zeros_like(f)
+        it, hist = s.solve(x, f, tol=0.0, maxit=8)
+        s.close()
+        assert all(b < a for a, b in zip(hist, hist[1:])), (inner, hist)
+        rates[inner] = (hist[-1] / hist[2]) ** (1.0 / (len(hist) - 3))
+        del x
+    print("c5 per-cycle rates", rates)
+    assert rates["jacobi"] < 0.97 and rates["mg"] < 0.75 and rates["mg"] < rates["jacobi"]

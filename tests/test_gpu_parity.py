@@ -221,3 +221,29 @@ def test_deterministic(torch_cuda):
         x = torch.zeros_like(f)
         outs.append((s.solve(x, f, tol=1e-8, maxit=5), x.clone()))
     assert outs[0][0] == outs[1][0] and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("inner", ["jacobi", "mg"])
+def test_graph_replay_bitwise(torch_cuda, inner):
+    # st_set_graphs: the captured launch sequence is the same kernels on the same pointers, so the
+    # results are bitwise those of direct launches; a new (x, f) pair captures its own graph
+    torch = torch_cuda
+    w = workloads.small("c2_lam10")
+    f = torch.from_numpy(w.rhs()).cuda()
+    outs = []
+    for graphs in (False, True):
+        s = solver(w, inner=inner)
+        s.set_graphs(graphs)
+        x = torch.zeros_like(f)
+        l0 = s.info()["kernel_launches"]
+        it, h = s.solve(x, f, tol=0.0, maxit=4)
+        launches = s.info()["kernel_launches"] - l0
+        x2 = torch.ones_like(f)
+        s.vcycle(x2, f)
+        s.vcycle(x2, f)
+        torch.cuda.synchronize()
+        outs.append((x.cpu().numpy(), h, x2.cpu().numpy(), launches))
+        s.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
+    assert np.array_equal(outs[0][2], outs[1][2])
+    assert outs[0][3] == outs[1][3] > 0
