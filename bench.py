@@ -297,7 +297,7 @@ def run_ours(args, rank, world, local_rank):
     if args.profile_out:
         with open(args.profile_out, "w") as fh:
             json.dump(out, fh, indent=1)
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
 
 
 def main():

@@ -55,6 +55,7 @@ struct st_handle {
     int64_t n_dofs = 0;
     // CUDA-graph replay of the single-process V-cycle (st_set_graphs)
     bool use_graphs = false;
+    bool gtr_two_pass = true;   // env ST_GTR_TWO_PASS=0: always the fused node-row G^T M kernel
     cudaStream_t cap_stream = nullptr;
     struct Graph { const double *x, *f; cudaGraphExec_t exec; int64_t launches; };
     std::vector<Graph> graphs;
@@ -243,9 +244,17 @@ void correct_A_local(st_handle *h, DevLevel &L, double *x, const double *f, cons
     auto s = (st::Stream)h->stream;
     const int Q = h->Q;
     const double ev = evec(L, Q), nv = nvec(L, Q), kb = ell_bytes(L.Kn) + 8.0 * L.n_nodes;
-    // fused nodal residual: w = G^T (f - L x) by a node-row SpMV with G^T M (K G = 0), zn = omega_n w / d_n
-    h->run("gtr", 2 * ev + (o.nu_n > 2 ? 2 : 1) * nv + ell_bytes(L.GtM) + 8.0 * L.n_nodes, 1,
-           [&] { st::launch_gtr(s, L, h->kt, Q, x, f, prev, o.omega_n, L.zn, o.nu_n > 2 ? L.wn : nullptr); });
+    if (h->gtr_two_pass && L.M.width <= 12) {
+        // narrow M (uniform meshes): u = f - (Ct (x) M) x + coupling on edge rows, then w = G^T u
+        // on node rows (6 gathers) -- one more vector pass, far fewer L1 gathers than G^T M
+        h->run("gtr_mass", 3 * ev + ell_bytes(L.M), 1, [&] { st::launch_res_mass(s, L, h->kt, Q, x, f, prev, L.r); });
+        h->run("gt", ev + (o.nu_n > 2 ? 2 : 1) * nv + 8.0 * L.n_nodes, 1,
+               [&] { st::launch_gt(s, L, Q, L.r, o.omega_n, L.zn, o.nu_n > 2 ? L.wn : nullptr); });
+    } else {
+        // fused nodal residual: w = G^T (f - L x) by a node-row SpMV with G^T M (K G = 0), zn = omega_n w / d_n
+        h->run("gtr", 2 * ev + (o.nu_n > 2 ? 2 : 1) * nv + ell_bytes(L.GtM) + 8.0 * L.n_nodes, 1,
+               [&] { st::launch_gtr(s, L, h->kt, Q, x, f, prev, o.omega_n, L.zn, o.nu_n > 2 ? L.wn : nullptr); });
+    }
     double *cur = L.zn, *other = L.zn2;
     int mode = o.nu_n == 1 ? 0 : (o.nu_n == 2 ? 1 : 2);
     for (int i = 2; i < o.nu_n; ++i) {
@@ -464,6 +473,7 @@ int st_setup(const st_params *p, st_handle **out) {
         ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
         h->own_stream = true;
         if (const char *dbg = std::getenv("ST_DEBUG_SYNC")) h->debug_sync = dbg[0] == '1';
+        if (const char *tp = std::getenv("ST_GTR_TWO_PASS")) h->gtr_two_pass = tp[0] != '0';
         size_t max_partial = 1;
         auto build = [&](int l, int b, int cnt, bool coarsest, bool alloc_x) {
             st::HostLevel &H = h->hl[l];
@@ -695,8 +705,10 @@ int st_profile(st_handle *h, int enable) {
     if (!h) return fail(1, "null handle");
     ST_GUARD({
         ck(cudaStreamSynchronize(h->stream), "sync");
-        for (auto &r : h->recs) { h->pool.push_back(r.a); h->pool.push_back(r.b); }
-        if (enable) h->recs.clear();
+        if (enable) {   // a fresh record: recycle the old events (recs and pool stay disjoint)
+            for (auto &r : h->recs) { h->pool.push_back(r.a); h->pool.push_back(r.b); }
+            h->recs.clear();
+        }
         h->prof = enable != 0;
     })
 }

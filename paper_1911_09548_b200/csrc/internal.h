@@ -147,6 +147,9 @@ void launch_end_values(Stream st, int rows, int Q, int S, const double *x, doubl
 void launch_restrict(Stream st, const DevLevel &F, const DevLevel &C, int Q, const double *r, double *fc);
 void launch_prolong(Stream st, const DevLevel &F, int Q, const double *xc, double *x);
 int launch_coarsest(Stream st, const DevLevel &L, int Q, const double *f, double *x);
+void launch_res_mass(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
+                     const double *prev, double *u);
+void launch_gt(Stream st, const DevLevel &L, int Q, const double *u, double omega_n, double *zn, double *w);
 void launch_residual_local(Stream st, const DevLevel &L, const KT &kt, int Q, const double *z, const double *r,
                            double *d);
 void launch_nodal_step(Stream st, const DevLevel &L, const KT &kt, int Q, const double *r, const double *z,

@@ -427,6 +427,97 @@ __global__ void __launch_bounds__(kBlock) k_axpy(size_t n, double alpha, const d
     if (i < n) x[i] += alpha * z[i];
 }
 
+// ------------------------------------------------- two-pass nodal residual
+// Pass 1 (edge rows): u = f - (Ct (x) M) x + (Nt (x) M) x_prev, the residual without K
+// (G^T K = 0, so G^T u = G^T (f - L x)).  Pays off where M is narrow (9 slots on uniform
+// hexes against 54 for the node-row G^T M of k_gtr): fewer L1 gathers for one more vector pass.
+template <int Q, int SPL, int WM>
+__global__ void __launch_bounds__(kBlock) k_res_mass(BoxMap m, DevELL M, const double *__restrict__ x,
+                                                     const double *__restrict__ f, const double *__restrict__ prev,
+                                                     double *__restrict__ u, KT kt) {
+    box_loop(m, [&](int row, int k0, bool valid) {
+        const int S = m.S;
+        const size_t QS = (size_t)Q * S;
+        double mx[Q][SPL], mp[SPL];
+#pragma unroll
+        for (int a = 0; a < Q; ++a)
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) mx[a][j] = 0.0;
+        const int wm = WM > 0 ? WM : M.width;
+        const Ent *eM = M.e + (size_t)row * wm;
+#pragma unroll (WM > 0 ? WM : 3)
+        for (int s = 0; s < wm; ++s) {
+            double v; int c;
+            ld_ent(eM + s, v, c);
+            const double *xc = x + (size_t)c * QS + k0;
+#pragma unroll
+            for (int a = 0; a < Q; ++a) {
+                double xv[SPL];
+                ldv<SPL>(xc + a * S, xv);
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) mx[a][j] = fma(v, xv[j], mx[a][j]);
+            }
+        }
+        coupling<Q, SPL, WM>(M, row, k0, S, 1 << m.lpr_log2, x, prev, mx, mp);
+        if (!valid) return;
+        const size_t base = (size_t)row * QS + k0;
+#pragma unroll
+        for (int b = 0; b < Q; ++b) {
+            double fv[SPL], uv[SPL];
+            ldv<SPL>(f + base + b * S, fv);
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) {
+                double acc = 0.0;
+#pragma unroll
+                for (int a = 0; a < Q; ++a) acc += kt.Ct[b * Q + a] * mx[a][j];
+                uv[j] = fv[j] - acc + (b == 0 ? mp[j] : 0.0);
+            }
+            stv<SPL>(u + base + b * S, uv);
+        }
+    });
+}
+
+// Pass 2 (node rows): w = G^T u, zn = omega_n w / d_n (w stored for nu_n > 2)
+template <int Q, int SPL, bool W_OUT>
+__global__ void __launch_bounds__(kBlock) k_gt(BoxMap m, DevELL GT, const double *__restrict__ u,
+                                               const double *__restrict__ dN, double omega_n,
+                                               double *__restrict__ zn, double *__restrict__ w) {
+    box_loop(m, [&](int node, int k0, bool valid) {
+        if (!valid) return;
+        const int S = m.S;
+        const size_t QS = (size_t)Q * S;
+        double g[Q][SPL];
+#pragma unroll
+        for (int a = 0; a < Q; ++a)
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) g[a][j] = 0.0;
+        const int *gc = GT.col + (size_t)node * GT.width;
+        for (int s = 0; s < GT.width; ++s) {
+            const int code = __ldg(gc + s);
+            if (code < 0) break;
+            const double sg = (code & 1) ? -1.0 : 1.0;
+            const double *ue = u + (size_t)(code >> 1) * QS + k0;
+#pragma unroll
+            for (int a = 0; a < Q; ++a) {
+                double uv[SPL];
+                ldv<SPL>(ue + a * S, uv);
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) g[a][j] = fma(sg, uv[j], g[a][j]);
+            }
+        }
+        const double inv = omega_n / __ldg(dN + node);
+        const size_t base = (size_t)node * QS + k0;
+#pragma unroll
+        for (int a = 0; a < Q; ++a) {
+            double zv[SPL];
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) zv[j] = g[a][j] * inv;
+            stv<SPL>(zn + base + a * S, zv);
+            if (W_OUT) stv<SPL>(w + base + a * S, g[a]);
+        }
+    });
+}
+
 // ------------------------------------------------------- nodal correction
 // Fused nodal residual (first half of Eq. 5): w = G^T (f - L x) computed per node without the
 // edge residual: G^T K = 0, so w = G^T f - sum_a Ct[b][a] (G^T M x_a) + e_0 (G^T M x_q)(k-1);
@@ -1225,6 +1316,24 @@ void launch_gtr(Stream st, const DevLevel &L, const KT &kt, int Q, const double 
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, {
         if (w) k_gtr<QQ, SP, true><<<grid(m), kBlock, 0, st>>>(m, L.GT, L.GtM, x, f, prev, L.dN, omega_n, kt, zn, w);
         else k_gtr<QQ, SP, false><<<grid(m), kBlock, 0, st>>>(m, L.GT, L.GtM, x, f, prev, L.dN, omega_n, kt, zn, w);
+    }));
+}
+
+void launch_res_mass(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
+                     const double *prev, double *u) {
+    const BoxMap m = edge_map(L);
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, {
+        if (L.M.width == 9) k_res_mass<QQ, SP, 9><<<grid(m), kBlock, 0, st>>>(m, L.M, x, f, prev, u, kt);
+        else if (L.M.width == 3) k_res_mass<QQ, SP, 3><<<grid(m), kBlock, 0, st>>>(m, L.M, x, f, prev, u, kt);
+        else k_res_mass<QQ, SP, 0><<<grid(m), kBlock, 0, st>>>(m, L.M, x, f, prev, u, kt);
+    }));
+}
+
+void launch_gt(Stream st, const DevLevel &L, int Q, const double *u, double omega_n, double *zn, double *w) {
+    const BoxMap m = make_boxmap(L.S, L.sched_n, L.bptr_n, L.nbox_n, L.lpr_log2);
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, {
+        if (w) k_gt<QQ, SP, true><<<grid(m), kBlock, 0, st>>>(m, L.GT, u, L.dN, omega_n, zn, w);
+        else k_gt<QQ, SP, false><<<grid(m), kBlock, 0, st>>>(m, L.GT, u, L.dN, omega_n, zn, w);
     }));
 }
 
