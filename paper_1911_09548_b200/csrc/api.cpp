@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -55,7 +56,9 @@ struct st_handle {
     int64_t n_dofs = 0;
     // CUDA-graph replay of the single-process V-cycle (st_set_graphs)
     bool use_graphs = false;
-    bool gtr_two_pass = true;   // env ST_GTR_TWO_PASS=0: always the fused node-row G^T M kernel
+    bool gtr_two_pass = true;
+    bool mk_dict = true;        // env ST_MK_DICT=0: never use the dictionary ELL
+    std::vector<int> tab_slots;   // env ST_GTR_TWO_PASS=0: always the fused node-row G^T M kernel
     cudaStream_t cap_stream = nullptr;
     struct Graph { const double *x, *f; cudaGraphExec_t exec; int64_t launches; };
     std::vector<Graph> graphs;
@@ -131,8 +134,44 @@ struct st_handle {
         }
         return d;
     }
+    // merged M/K operator of a level: (col, (M, K)) ELL, plus the dictionary form when the level
+    // has a uniform stencil width (33 in 3D, 7 in 2D) and at most 256 distinct (M, K) pairs
+    void upload_mk(const st::HostELL &MK, const std::vector<double> &MKk, int m_width, st::DevLevel &D) {
+        std::vector<double2> mkv(MK.val.size());
+        for (size_t i = 0; i < mkv.size(); ++i) mkv[i] = make_double2(MK.val[i], MKk[i]);
+        D.mk_width = MK.width;
+        D.mk_col = upload(MK.col);
+        D.mk_val = upload(mkv);
+        const bool stencil = (m_width == 9 && MK.width == 33) || (m_width == 3 && MK.width == 7);
+        if (!mk_dict || !stencil || MK.rows >= (1 << 24)) return;
+        std::map<std::pair<uint64_t, uint64_t>, unsigned> ids;
+        std::vector<double2> tab;
+        const int W = MK.width, W4 = (W + 3) / 4 * 4;
+        std::vector<unsigned> pk((size_t)MK.rows * W4, 0u);
+        for (int r = 0; r < MK.rows; ++r)
+            for (int s = 0; s < W; ++s) {
+                const size_t i = (size_t)r * W + s;
+                uint64_t a, b;
+                std::memcpy(&a, &MK.val[i], 8);
+                std::memcpy(&b, &MKk[i], 8);
+                auto it = ids.find({a, b});
+                if (it == ids.end()) {
+                    if (tab.size() == 256) return;        // too many distinct values: plain ELL
+                    it = ids.emplace(std::make_pair(a, b), (unsigned)tab.size()).first;
+                    tab.push_back(mkv[i]);
+                }
+                if (MK.col[i] < 0) return;
+                pk[(size_t)r * W4 + s] = ((unsigned)MK.col[i] << 8) | it->second;
+            }
+        const int off = st::acquire_mk_table(tab.data(), (int)tab.size());
+        if (off < 0) return;
+        tab_slots.push_back(off);
+        D.mk_pk = upload(pk);
+        D.mk_tab = off;
+    }
     ~st_handle() {
         clear_graphs();
+        for (int t : tab_slots) st::release_mk_table(t);
         if (cap_stream) cudaStreamDestroy(cap_stream);
         for (auto &r : recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
         for (auto e : pool) cudaEventDestroy(e);
@@ -474,6 +513,7 @@ int st_setup(const st_params *p, st_handle **out) {
         h->own_stream = true;
         if (const char *dbg = std::getenv("ST_DEBUG_SYNC")) h->debug_sync = dbg[0] == '1';
         if (const char *tp = std::getenv("ST_GTR_TWO_PASS")) h->gtr_two_pass = tp[0] != '0';
+        if (const char *md = std::getenv("ST_MK_DICT")) h->mk_dict = md[0] != '0';
         size_t max_partial = 1;
         auto build = [&](int l, int b, int cnt, bool coarsest, bool alloc_x) {
             st::HostLevel &H = h->hl[l];
@@ -483,13 +523,7 @@ int st_setup(const st_params *p, st_handle **out) {
                 throw Unsupported("level too large for 32-bit thread indexing");
             D.M = h->upload(H.M); D.K = h->upload(H.K); D.Kn = h->upload(H.Kn); D.GT = h->upload(H.GT);
             D.GtM = h->upload(H.GtM);
-            {
-                std::vector<double2> mkv(H.MK.val.size());
-                for (size_t i = 0; i < mkv.size(); ++i) mkv[i] = make_double2(H.MK.val[i], H.MKk[i]);
-                D.mk_width = H.MK.width;
-                D.mk_col = h->upload(H.MK.col);
-                D.mk_val = h->upload(mkv);
-            }
+            h->upload_mk(H.MK, H.MKk, H.M.width, D);
             D.dM = h->upload(H.dM); D.dK = h->upload(H.dK); D.dN = h->upload(H.dN);
             D.edge_nodes = h->upload(H.mesh.edge_nodes);
             D.sched_e = h->upload(H.sched_e); D.bptr_e = h->upload(H.bptr_e);
@@ -547,9 +581,7 @@ int st_setup(const st_params *p, st_handle **out) {
                 DevLevel D;
                 D.n_edges = C.mesh.n_edges; D.n_nodes = C.mesh.n_nodes; D.Q = Q;
                 D.M = h->upload(C.M); D.K = h->upload(C.K); D.GT = h->upload(C.GT); D.GtM = h->upload(C.GtM);
-                std::vector<double2> mkv(C.MK.val.size());
-                for (size_t i = 0; i < mkv.size(); ++i) mkv[i] = make_double2(C.MK.val[i], C.MKk[i]);
-                D.mk_width = C.MK.width; D.mk_col = h->upload(C.MK.col); D.mk_val = h->upload(mkv);
+                h->upload_mk(C.MK, C.MKk, C.M.width, D);
                 D.dM = h->upload(C.dM); D.dK = h->upload(C.dK); D.dN = h->upload(C.dN);
                 D.edge_nodes = h->upload(C.mesh.edge_nodes);
                 D.sched_e = h->upload(C.sched_e); D.bptr_e = h->upload(C.bptr_e);

@@ -87,6 +87,8 @@ struct DevLevel {
     int mk_width = 0;
     int *mk_col = nullptr;          // [row][slot] union columns of M and K
     double2 *mk_val = nullptr;      // [row][slot] (M value, K value)
+    unsigned *mk_pk = nullptr;      // dictionary form: [row][slot (width padded to 4)] col << 8 | value id, or null
+    int mk_tab = 0;                 // offset of this level's value table in the constant bank
     double *dM = nullptr, *dK = nullptr, *dN = nullptr;
     int *edge_nodes = nullptr;
     int *sched_e = nullptr, *bptr_e = nullptr, *sched_n = nullptr, *bptr_n = nullptr;
@@ -147,6 +149,8 @@ void launch_end_values(Stream st, int rows, int Q, int S, const double *x, doubl
 void launch_restrict(Stream st, const DevLevel &F, const DevLevel &C, int Q, const double *r, double *fc);
 void launch_prolong(Stream st, const DevLevel &F, int Q, const double *xc, double *x);
 int launch_coarsest(Stream st, const DevLevel &L, int Q, const double *f, double *x);
+int acquire_mk_table(const double2 *vals, int n);   // -1: no free constant-bank slot
+void release_mk_table(int offset);
 void launch_res_mass(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
                      const double *prev, double *u);
 void launch_gt(Stream st, const DevLevel &L, int Q, const double *u, double omega_n, double *zn, double *w);

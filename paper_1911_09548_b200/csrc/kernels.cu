@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <mutex>
 #include <stdexcept>
 
 #include "internal.h"
@@ -219,13 +220,37 @@ __device__ __forceinline__ void spatial_apply(const DevELL &M, const DevELL &K, 
 }
 
 // Merged M/K ELL: one column list, (M value, K value) pairs; one gather feeds both products.
+// Dictionary form (levels whose operator has at most kTabSize distinct (M, K) pairs, e.g.
+// uniform meshes with piecewise-constant coefficients): entry = col << 8 | value id, rows padded
+// to a multiple of 4 entries and read 4 at a time, values from the constant bank (warp-uniform
+// index: served by the constant cache, not the L1 data pipe that bounds these kernels).
 struct MKELL {
     const int *col;
     const double2 *val;
     int width;
+    const unsigned *pk = nullptr;
+    int tab = 0;
 };
 
-template <int Q, int SPL, int W>
+constexpr int kTabSize = 256, kTabSlots = 14;
+__constant__ double2 c_mk_tab[kTabSize * kTabSlots];
+
+template <int Q, int SPL>
+__device__ __forceinline__ void mk_fma(const double2 v, const double *__restrict__ xc, int S,
+                                       double (&mx)[Q][SPL], double (&kx)[Q][SPL]) {
+#pragma unroll
+    for (int a = 0; a < Q; ++a) {
+        double xv[SPL];
+        ldv<SPL>(xc + a * S, xv);
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+            mx[a][j] = fma(v.x, xv[j], mx[a][j]);
+            kx[a][j] = fma(v.y, xv[j], kx[a][j]);
+        }
+    }
+}
+
+template <int Q, int SPL, int W, bool DICT = false>
 __device__ __forceinline__ void spatial_apply_mk(const MKELL &A, int row, int k0, int S,
                                                  const double *__restrict__ x,
                                                  double (&mx)[Q][SPL], double (&kx)[Q][SPL]) {
@@ -234,6 +259,23 @@ __device__ __forceinline__ void spatial_apply_mk(const MKELL &A, int row, int k0
     for (int a = 0; a < Q; ++a)
 #pragma unroll
         for (int j = 0; j < SPL; ++j) { mx[a][j] = 0.0; kx[a][j] = 0.0; }
+    if (DICT) {
+        static_assert(!DICT || W > 0, "dictionary ELL needs a compile-time width");
+        constexpr int W4 = (W + 3) / 4 * 4;
+        const uint4 *pp = reinterpret_cast<const uint4 *>(A.pk + (size_t)row * W4);
+#pragma unroll
+        for (int s0 = 0; s0 < W; s0 += 4) {
+            const uint4 e4 = __ldg(pp + s0 / 4);
+            const unsigned es[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (s0 + t < W) {
+                    const double2 v = c_mk_tab[A.tab + (es[t] & 255u)];
+                    mk_fma<Q, SPL>(v, x + (size_t)(es[t] >> 8) * QS + k0, S, mx, kx);
+                }
+        }
+        return;
+    }
     const int w = W > 0 ? W : A.width;
     const int *cc = A.col + (size_t)row * w;
     const double2 *vv = A.val + (size_t)row * w;
@@ -241,17 +283,7 @@ __device__ __forceinline__ void spatial_apply_mk(const MKELL &A, int row, int k0
     for (int s = 0; s < w; ++s) {
         const int c = __ldg(cc + s);
         const double2 v = __ldg(vv + s);
-        const double *xc = x + (size_t)c * QS + k0;
-#pragma unroll
-        for (int a = 0; a < Q; ++a) {
-            double xv[SPL];
-            ldv<SPL>(xc + a * S, xv);
-#pragma unroll
-            for (int j = 0; j < SPL; ++j) {
-                mx[a][j] = fma(v.x, xv[j], mx[a][j]);
-                kx[a][j] = fma(v.y, xv[j], kx[a][j]);
-            }
-        }
+        mk_fma<Q, SPL>(v, x + (size_t)c * QS + k0, S, mx, kx);
     }
 }
 
@@ -292,7 +324,7 @@ __device__ __forceinline__ void coupling(const DevELL &M, int row, int k0, int S
 // ------------------------------------------------------------ residual
 // r = f - L x; optionally z = omega_s D^{-1} r (first Jacobi sweep of B from zero)
 // and per-block partial sums of |r|^2.
-template <int Q, int SPL, int WM, int WK, bool R_OUT, bool Z_OUT, bool NORM, bool COUPLE = true>
+template <int Q, int SPL, int WM, int WK, bool R_OUT, bool Z_OUT, bool NORM, bool COUPLE = true, bool DICT = false>
 __global__ void __launch_bounds__(kBlock) k_residual(BoxMap m, DevELL M, MKELL MK, const double *__restrict__ tau,
                                                      const double *__restrict__ x, const double *__restrict__ f,
                                                      const double *__restrict__ prev, double *__restrict__ r,
@@ -303,7 +335,7 @@ __global__ void __launch_bounds__(kBlock) k_residual(BoxMap m, DevELL M, MKELL M
     box_loop(m, [&](int row, int k0, bool valid) {
         const int S = m.S;
         double mx[Q][SPL], kx[Q][SPL], mp[SPL];
-        spatial_apply_mk<Q, SPL, WK>(MK, row, k0, S, x, mx, kx);
+        spatial_apply_mk<Q, SPL, WK, DICT>(MK, row, k0, S, x, mx, kx);
         if (COUPLE) coupling<Q, SPL, WM>(M, row, k0, S, 1 << m.lpr_log2, x, prev, mx, mp);
         else
 #pragma unroll
@@ -361,7 +393,7 @@ __global__ void __launch_bounds__(kBlock) k_residual(BoxMap m, DevELL M, MKELL M
 // right after the fused first one, reconstructed pointwise as r = D z / omega_s.
 // LAST: x += omega * znew (the smoother update of Eq. 2), in place (x is only
 // read at its own row).
-template <int Q, int SPL, int WM, int WK, bool LAST, bool RECON>
+template <int Q, int SPL, int WM, int WK, bool LAST, bool RECON, bool DICT = false>
 __global__ void __launch_bounds__(kBlock) k_sweep(BoxMap m, DevELL M, MKELL MK, const double *__restrict__ tau,
                                                   const double *__restrict__ dM, const double *__restrict__ dK,
                                                   const double *__restrict__ z, const double *__restrict__ r,
@@ -369,7 +401,7 @@ __global__ void __launch_bounds__(kBlock) k_sweep(BoxMap m, DevELL M, MKELL MK, 
     box_loop(m, [&](int row, int k0, bool valid) {
     const int S = m.S;
     double mz[Q][SPL], kz[Q][SPL];
-    spatial_apply_mk<Q, SPL, WK>(MK, row, k0, S, z, mz, kz);
+    spatial_apply_mk<Q, SPL, WK, DICT>(MK, row, k0, S, z, mz, kz);
     if (!valid) return;
     double t[SPL];
     ldv<SPL>(tau + k0, t);
@@ -432,7 +464,7 @@ __global__ void __launch_bounds__(kBlock) k_axpy(size_t n, double alpha, const d
 // (G^T K = 0, so G^T u = G^T (f - L x)).  Pays off where M is narrow (9 slots on uniform
 // hexes against 54 for the node-row G^T M of k_gtr): fewer L1 gathers for one more vector pass.
 template <int Q, int SPL, int WM>
-__global__ void __launch_bounds__(kBlock) k_res_mass(BoxMap m, DevELL M, const double *__restrict__ x,
+__global__ void __launch_bounds__(kBlock, 4) k_res_mass(BoxMap m, DevELL M, const double *__restrict__ x,
                                                      const double *__restrict__ f, const double *__restrict__ prev,
                                                      double *__restrict__ u, KT kt) {
     box_loop(m, [&](int row, int k0, bool valid) {
@@ -1223,11 +1255,13 @@ static inline BoxMap node_map(const DevLevel &L) { return make_boxmap(L.S, L.sch
 // compile-time ELL widths of the common stencils: uniform hexes (9, 33), general hexes
 // (33, 33), uniform quads (3, 7), general quads (7, 7); anything else runtime
 #define ST_DISPATCH_W(wm, wk, ...)                                                        \
-    if (wm == 9 && wk == 33) { constexpr int WM_ = 9, WK_ = 33; __VA_ARGS__; }           \
-    else if (wm == 33 && wk == 33) { constexpr int WM_ = 33, WK_ = 33; __VA_ARGS__; }    \
-    else if (wm == 3 && wk == 7) { constexpr int WM_ = 3, WK_ = 7; __VA_ARGS__; }        \
-    else if (wm == 7 && wk == 7) { constexpr int WM_ = 7, WK_ = 7; __VA_ARGS__; }        \
-    else { constexpr int WM_ = 0, WK_ = 0; __VA_ARGS__; }
+    if (wm == 9 && wk == 33 && MK.pk) { constexpr int WM_ = 9, WK_ = 33; constexpr bool DI_ = true; __VA_ARGS__; } \
+    else if (wm == 3 && wk == 7 && MK.pk) { constexpr int WM_ = 3, WK_ = 7; constexpr bool DI_ = true; __VA_ARGS__; } \
+    else if (wm == 9 && wk == 33) { constexpr int WM_ = 9, WK_ = 33; constexpr bool DI_ = false; __VA_ARGS__; } \
+    else if (wm == 33 && wk == 33) { constexpr int WM_ = 33, WK_ = 33; constexpr bool DI_ = false; __VA_ARGS__; } \
+    else if (wm == 3 && wk == 7) { constexpr int WM_ = 3, WK_ = 7; constexpr bool DI_ = false; __VA_ARGS__; } \
+    else if (wm == 7 && wk == 7) { constexpr int WM_ = 7, WK_ = 7; constexpr bool DI_ = false; __VA_ARGS__; } \
+    else { constexpr int WM_ = 0, WK_ = 0; constexpr bool DI_ = false; __VA_ARGS__; }
 
 static MarchMap march_map(const DevLevel &L, bool halo) {
     MarchMap mm{};
@@ -1261,17 +1295,17 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
     }
     const BoxMap m = edge_map(L);
     const int g = grid(m);
-    const MKELL MK{L.mk_col, L.mk_val, L.mk_width};
+    const MKELL MK{L.mk_col, L.mk_val, L.mk_width, L.mk_pk, L.mk_tab};
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.mk_width, {
         if (partial) {
-            if (r) k_residual<QQ, SP, WM_, WK_, true, false, true><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
-            else k_residual<QQ, SP, WM_, WK_, false, false, true><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            if (r) k_residual<QQ, SP, WM_, WK_, true, false, true, true, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            else k_residual<QQ, SP, WM_, WK_, false, false, true, true, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         } else if (r && z) {
-            k_residual<QQ, SP, WM_, WK_, true, true, false><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            k_residual<QQ, SP, WM_, WK_, true, true, false, true, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         } else if (z) {
-            k_residual<QQ, SP, WM_, WK_, false, true, false><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            k_residual<QQ, SP, WM_, WK_, false, true, false, true, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         } else {
-            k_residual<QQ, SP, WM_, WK_, true, false, false><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
+            k_residual<QQ, SP, WM_, WK_, true, false, false, true, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
         }
     })));
     return g;
@@ -1296,12 +1330,14 @@ void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, 
     }
     const BoxMap m = edge_map(L, 4);   // 4 slabs per lane: measured faster for the sweep (not the residual)
     const int g = grid(m);
+    // the dictionary ELL is not used here: measured 13 % slower for this 4-slab, 128-register
+    // kernel (3 % faster for the residual)
     const MKELL MK{L.mk_col, L.mk_val, L.mk_width};
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL4(m.spl, ST_DISPATCH_W(L.M.width, L.mk_width, {
-        if (last && recon) k_sweep<QQ, SP, WM_, WK_, true, true><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
-        else if (last) k_sweep<QQ, SP, WM_, WK_, true, false><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
-        else if (recon) k_sweep<QQ, SP, WM_, WK_, false, true><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
-        else k_sweep<QQ, SP, WM_, WK_, false, false><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+        if (last && recon) k_sweep<QQ, SP, WM_, WK_, true, true, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+        else if (last) k_sweep<QQ, SP, WM_, WK_, true, false, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+        else if (recon) k_sweep<QQ, SP, WM_, WK_, false, true, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
+        else k_sweep<QQ, SP, WM_, WK_, false, false, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
     })));
 }
 
@@ -1385,13 +1421,35 @@ void launch_prolong(Stream st, const DevLevel &F, int Q, const double *xc, doubl
     });
 }
 
+// constant-bank slots for dictionary ELL tables (shared by all handles of the process)
+static std::mutex g_tab_mu;
+static bool g_tab_used[kTabSlots];
+
+int acquire_mk_table(const double2 *vals, int n) {
+    if (n > kTabSize) return -1;
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    for (int s = 0; s < kTabSlots; ++s)
+        if (!g_tab_used[s]) {
+            if (cudaMemcpyToSymbol(c_mk_tab, vals, sizeof(double2) * n, sizeof(double2) * s * kTabSize) != cudaSuccess)
+                return -1;
+            g_tab_used[s] = true;
+            return s * kTabSize;
+        }
+    return -1;
+}
+
+void release_mk_table(int offset) {
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    if (offset >= 0 && offset / kTabSize < kTabSlots) g_tab_used[offset / kTabSize] = false;
+}
+
 // inner spatial V-cycle pieces (R13)
 void launch_residual_local(Stream st, const DevLevel &L, const KT &kt, int Q, const double *z, const double *r,
                            double *d) {
     const BoxMap m = edge_map(L);
-    const MKELL MK{L.mk_col, L.mk_val, L.mk_width};
+    const MKELL MK{L.mk_col, L.mk_val, L.mk_width, L.mk_pk, L.mk_tab};
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.mk_width, {
-        k_residual<QQ, SP, WM_, WK_, true, false, false, false><<<grid(m), kBlock, 0, st>>>(m, L.M, MK, L.tau, z, r, nullptr, d, nullptr, L.dM, L.dK, 0.0, kt, nullptr);
+        k_residual<QQ, SP, WM_, WK_, true, false, false, false, DI_><<<grid(m), kBlock, 0, st>>>(m, L.M, MK, L.tau, z, r, nullptr, d, nullptr, L.dM, L.dK, 0.0, kt, nullptr);
     })));
 }
 
