@@ -1328,11 +1328,15 @@ void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, 
         });
         return;
     }
-    const BoxMap m = edge_map(L, 4);   // 4 slabs per lane: measured faster for the sweep (not the residual)
+    // Plain ELL: 4 slabs per lane (measured faster than 2 for the sweep, not for the residual).
+    // Dictionary ELL (stencil levels): 2 slabs per lane, measured 305 vs 354 ms per 5 V-cycles
+    // on c4 (the dictionary at 4 slabs per lane, 128 registers, was 13 % slower).
+    // Env ST_SWEEP_DICT=0 forces the plain form (measurements).
+    static const bool no_dict = std::getenv("ST_SWEEP_DICT") && std::getenv("ST_SWEEP_DICT")[0] == '0';
+    const bool dict = L.mk_pk && !no_dict;
+    const BoxMap m = edge_map(L, dict ? 2 : 4);
     const int g = grid(m);
-    // the dictionary ELL is not used here: measured 13 % slower for this 4-slab, 128-register
-    // kernel (3 % faster for the residual)
-    const MKELL MK{L.mk_col, L.mk_val, L.mk_width};
+    const MKELL MK{L.mk_col, L.mk_val, L.mk_width, dict ? L.mk_pk : nullptr, L.mk_tab};
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL4(m.spl, ST_DISPATCH_W(L.M.width, L.mk_width, {
         if (last && recon) k_sweep<QQ, SP, WM_, WK_, true, true, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
         else if (last) k_sweep<QQ, SP, WM_, WK_, true, false, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
