@@ -33,7 +33,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--slabs", type=int, default=512, help="slabs per GPU (weak scaling)")
-    ap.add_argument("--n", type=int, default=64, help="cells per direction")
+    ap.add_argument("--cells", type=int, default=64, help="cells per direction")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-out", default=None, help="write per-kernel event stats (json)")
@@ -44,11 +44,11 @@ def parse():
 
 
 def workload(args):
-    return workloads.c4(n=args.n, S=args.slabs, tau=1.0 / 4096)
+    return workloads.c4(n=args.cells, S=args.slabs, tau=1.0 / 4096)
 
 
 def workload_name(args):
-    return (f"c4: unit cube {args.n}^3 hex, lowest-order Nedelec, dG(1), tau=1/4096, sigma=nu=1, "
+    return (f"c4: unit cube {args.cells}^3 hex, lowest-order Nedelec, dG(1), tau=1/4096, sigma=nu=1, "
             f"{args.slabs} slabs per GPU, f ~ U(-1,1) seed 3"
             + ("" if args.inner == "jacobi" else ", inner spatial V-cycle for A_k^{-1} (R13)"))
 
@@ -182,14 +182,16 @@ def run_reference(args, rank, world):
 def run_ours(args, rank, world, local_rank):
     import torch
     import paper_1911_09548_b200 as p
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(local_rank % torch.cuda.device_count())
     dist = None
+    red_dev = "cuda"
     if world > 1:
         import torch.distributed as dist
+        red_dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
     # weak scaling: every rank owns `slabs` slabs of one global slab range (tau = 1/4096); with
     # N > 1 the V-cycle runs through paper_1911_09548_b200.distributed over NCCL (halo shift,
     # Sigma_t carries, coarse levels gathered on rank 0)
-    w = workloads.c4(n=args.n, S=args.slabs * world, tau=1.0 / 4096)
+    w = workloads.c4(n=args.cells, S=args.slabs * world, tau=1.0 / 4096)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         s = p.Solver.from_workload(w, stream=stream, rank=rank, nranks=world, kernel_path=args.kernel_path,
@@ -213,7 +215,7 @@ def run_ours(args, rank, world, local_rank):
         launches0 = s.info()["kernel_launches"]
         s.profile(True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local_rank) as clk:
+        with ClockSampler(local_rank % torch.cuda.device_count()) as clk:
             stream.synchronize()
             e0.record(stream)
             for _ in range(args.steps):
@@ -226,7 +228,7 @@ def run_ours(args, rank, world, local_rank):
         launches = s.info()["kernel_launches"] - launches0
         t_max = ms
         if dist:
-            t = torch.tensor([ms], device="cuda")
+            t = torch.tensor([ms], device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t_max = float(t.item())
         # end to end through the public API with host buffers: st_solve_host copies f and x in,
@@ -259,7 +261,7 @@ def run_ours(args, rank, world, local_rank):
                 te = (time.perf_counter() - t0) / ke
                 note = "per rank: H2D f,x from pinned memory, distributed V-cycle, D2H x"
             if dist:
-                t = torch.tensor([te], device="cuda", dtype=torch.float64)
+                t = torch.tensor([te], device=red_dev, dtype=torch.float64)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 te = float(t.item())
             e2e = {"value": n_dofs * world / te, "unit": UNIT, "h2d_bytes_per_step": 2 * f.numel() * 8 * world,
@@ -313,7 +315,9 @@ def main():
         return
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        # NCCL over NVLink; ST_BENCH_BACKEND=gloo only to exercise this path with several ranks
+        # on one GPU (host-staged messages; not a measurement configuration)
+        dist.init_process_group(os.environ.get("ST_BENCH_BACKEND", "nccl"))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
