@@ -110,10 +110,8 @@ def measured_peak():
 
 def ncu_traffic(family):
     """dram__bytes_read.sum + dram__bytes_write.sum of the finest-level launch of `family` from the
-    committed ncu --set full capture (profiles/r01_ncu_v5_kernels.json, else v4), or None."""
-    p = os.path.join(ROOT, "profiles", "r01_ncu_v5_kernels.json")
-    if not os.path.exists(p):
-        p = os.path.join(ROOT, "profiles", "r01_ncu_v4_kernels.json")
+    committed ncu --set full capture of the current kernels (profiles/r01_ncu_v6_kernels.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r01_ncu_v6_kernels.json")
     if not os.path.exists(p):
         return None
     tag = {"residual": "k_residual", "sweep_update": "k_sweep", "gtr": "k_gtr", "gtr_mass": "k_res_mass",
