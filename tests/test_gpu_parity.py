@@ -247,3 +247,50 @@ def test_graph_replay_bitwise(torch_cuda, inner):
     assert np.array_equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
     assert np.array_equal(outs[0][2], outs[1][2])
     assert outs[0][3] == outs[1][3] > 0
+
+
+@pytest.mark.parametrize("name,q", [("c4", 1), ("c4", 2), ("c2", 1), ("c1", 0)])
+def test_dictionary_ell_bitwise_equals_plain_ell(torch_cuda, name, q, monkeypatch):
+    # the dictionary ELL (packed entries, values from the constant bank) changes where the
+    # operands come from, not the arithmetic or its order: bitwise equal V-cycles and residuals
+    torch = torch_cuda
+    w = workloads.small(name)
+    w.q = q
+    rng = np.random.default_rng(51)
+    F = workloads.from_oracle(rng.uniform(-1, 1, (w.S, q + 1, w.n_edges)))
+    X0 = workloads.from_oracle(rng.uniform(-1, 1, (w.S, q + 1, w.n_edges)))
+    outs = []
+    for env in ({}, {"ST_MK_DICT": "0"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s = solver(w)
+        x = torch.from_numpy(X0).cuda()
+        f = torch.from_numpy(F).cuda()
+        s.vcycle(x, f)
+        r = torch.empty_like(f)
+        s.residual(x, f, r)
+        torch.cuda.synchronize()
+        outs.append((x.cpu().numpy(), r.cpu().numpy()))
+        s.close()
+        for k in env:
+            monkeypatch.delenv(k)
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_constant_bank_slots_exhausted_falls_back(torch_cuda):
+    # more live dictionary levels than constant-bank slots: later levels use the plain ELL and
+    # every handle still computes the same V-cycle
+    torch = torch_cuda
+    w = workloads.small("c4")
+    f = torch.from_numpy(w.rhs()).cuda()
+    live, outs = [], []
+    for _ in range(5):                  # 5 handles x 5 levels > 14 slots
+        s = solver(w)
+        x = torch.zeros_like(f)
+        s.vcycle(x, f)
+        live.append(s)
+        outs.append(x.cpu().numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    for s in live:
+        s.close()
