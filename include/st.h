@@ -133,6 +133,15 @@ int st_solve(st_handle *h, double *x, const double *f, double tol, int maxit,
 int st_solve_host(st_handle *h, double *x_host, const double *f_host, double tol,
                   int maxit, int *iters, double *hist);
 
+/* Streaming solve of n independent problems L x_i = f_i held in HOST memory (page-locked
+ * memory lets the copies overlap): each from x_i = 0, or from x_host[i] when init_from_x != 0,
+ * with st_solve's stopping rule.  Two device buffer pairs and two copy streams: the H2D copy of
+ * problem i+1 and the D2H copy of problem i-1 run while problem i is solved.  x_host[i] (out)
+ * is complete when the call returns.  iters (n ints) and hist (n * (maxit+1) doubles, problem
+ * i at hist + i*(maxit+1)) may be NULL.  Single-process handles only. */
+int st_solve_many_host(st_handle *h, int n, double *const *x_host, const double *const *f_host,
+                       int init_from_x, double tol, int maxit, int *iters, double *hist);
+
 int st_info(const st_handle *h, st_info_t *info);
 
 /* Per-kernel timing with CUDA events recorded on the handle's stream around

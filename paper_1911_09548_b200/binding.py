@@ -18,7 +18,7 @@ LEVEL_OPS = ["st_lv_count", "st_lv_get", "st_lv_residual", "st_lv_smooth_S", "st
              "st_lv_correct_apply", "st_lv_restrict", "st_lv_prolong", "st_lv_vcycle", "st_lv_end_values",
              "st_copy_slabs", "st_zero", "st_sync"]
 EXPORTED = ["st_setup", "st_free", "st_set_stream", "st_residual", "st_vcycle", "st_set_graphs", "st_solve",
-            "st_solve_host", "st_info", "st_profile", "st_profile_read", "st_plan", "st_host_matrix",
+            "st_solve_host", "st_solve_many_host", "st_info", "st_profile", "st_profile_read", "st_plan", "st_host_matrix",
             *LEVEL_OPS, "st_last_error"]
 
 
@@ -75,6 +75,8 @@ def load():
     lib.st_set_graphs.argtypes = [vp, ctypes.c_int]
     lib.st_solve.argtypes = [vp, vp, vp, ctypes.c_double, ctypes.c_int, ip, dp]
     lib.st_solve_host.argtypes = [vp, dp, dp, ctypes.c_double, ctypes.c_int, ip, dp]
+    lib.st_solve_many_host.argtypes = [vp, ctypes.c_int, ctypes.POINTER(dp), ctypes.POINTER(dp), ctypes.c_int,
+                                       ctypes.c_double, ctypes.c_int, ip, dp]
     lib.st_info.argtypes = [vp, ctypes.POINTER(StInfo)]
     lib.st_profile.argtypes = [vp, ctypes.c_int]
     lib.st_profile_read.argtypes = [vp, ctypes.POINTER(StKstat), ctypes.c_int, ip]
@@ -256,6 +258,22 @@ class Solver:
         hist = (ctypes.c_double * (maxit + 1))()
         _check(load().st_solve_host(self._h, _dptr(x), _dptr(f), tol, maxit, ctypes.byref(it), hist))
         return it.value, list(hist[: it.value + 1])
+
+    def solve_many_host(self, xs, fs, tol=1e-8, maxit=100, init_from_x=False):
+        """Streaming solves of independent problems (st_solve_many_host): xs (out, or in/out with
+        init_from_x) and fs are lists of host float64 arrays in ST layout (page-locked memory,
+        e.g. torch's pin_memory().numpy(), lets the copies overlap the solves).  Returns
+        (iterations, histories) per problem."""
+        n = len(fs)
+        assert len(xs) == n
+        for a in list(xs) + list(fs):
+            assert a.dtype == np.float64 and a.flags.c_contiguous and a.size == self.n_edges * (self.q + 1) * self.S
+        X = (ctypes.POINTER(ctypes.c_double) * n)(*[_dptr(a) for a in xs])
+        F = (ctypes.POINTER(ctypes.c_double) * n)(*[_dptr(a) for a in fs])
+        it = (ctypes.c_int * max(n, 1))()
+        hist = (ctypes.c_double * max(n * (maxit + 1), 1))()
+        _check(load().st_solve_many_host(self._h, n, X, F, 1 if init_from_x else 0, tol, maxit, it, hist))
+        return [it[i] for i in range(n)], [list(hist[i * (maxit + 1): i * (maxit + 1) + it[i] + 1]) for i in range(n)]
 
     # ---- level operations (multi-GPU driver: distributed.py) -------------------------
     def level(self, set_, level):

@@ -50,6 +50,10 @@ struct st_handle {
     int partial_cap = 0;
     double *dscal = nullptr;
     double *hx = nullptr, *hf = nullptr;   // device buffers for st_solve_host
+    // st_solve_many_host: double-buffered device problems, copy streams and their events
+    double *mx[2] = {nullptr, nullptr}, *mf[2] = {nullptr, nullptr};
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
     int64_t launches = 0;
     int64_t bytes = 0;
     std::vector<void *> allocs;
@@ -171,6 +175,11 @@ struct st_handle {
     }
     ~st_handle() {
         clear_graphs();
+        for (int b = 0; b < 2; ++b)
+            for (cudaEvent_t e : {ev_in[b], ev_done[b], ev_out[b]})
+                if (e) cudaEventDestroy(e);
+        if (h2d) cudaStreamDestroy(h2d);
+        if (d2h) cudaStreamDestroy(d2h);
         for (int t : tab_slots) st::release_mk_table(t);
         if (cap_stream) cudaStreamDestroy(cap_stream);
         for (auto &r : recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -728,6 +737,54 @@ int st_solve_host(st_handle *h, double *x_host, const double *f_host, double tol
         if (rc) throw CudaError(g_err);
         ck(cudaMemcpyAsync(x_host, h->hx, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "d2h x");
         ck(cudaStreamSynchronize(h->stream), "sync");
+    })
+}
+
+int st_solve_many_host(st_handle *h, int n, double *const *x_host, const double *const *f_host, int init_from_x,
+                       double tol, int maxit, int *iters, double *hist) {
+    if (!h || n < 0 || maxit < 0 || (n > 0 && (!x_host || !f_host))) return fail(1, "bad argument");
+    if (h->nranks > 1) return fail(1, "multi-rank handles solve through paper_1911_09548_b200.distributed");
+    for (int i = 0; i < n; ++i)
+        if (!x_host[i] || !f_host[i]) return fail(1, "null problem buffer");
+    ST_GUARD({
+        const size_t len = vec_len(h->dl[0], h->Q);
+        const size_t bytes = len * sizeof(double);
+        if (!h->mx[0]) {
+            for (int b = 0; b < 2; ++b) {
+                h->mx[b] = h->dalloc<double>(len);
+                h->mf[b] = h->dalloc<double>(len);
+                ck(cudaEventCreateWithFlags(&h->ev_in[b], cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&h->ev_done[b], cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&h->ev_out[b], cudaEventDisableTiming), "event");
+            }
+            ck(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking), "stream");
+        }
+        // buffer b is free for problem i once problem i-2's solve and D2H copy are done
+        auto load = [&](int i) {
+            const int b = i & 1;
+            ck(cudaStreamWaitEvent(h->h2d, h->ev_done[b], 0), "wait");
+            ck(cudaStreamWaitEvent(h->h2d, h->ev_out[b], 0), "wait");
+            ck(cudaMemcpyAsync(h->mf[b], f_host[i], bytes, cudaMemcpyHostToDevice, h->h2d), "h2d f");
+            if (init_from_x) ck(cudaMemcpyAsync(h->mx[b], x_host[i], bytes, cudaMemcpyHostToDevice, h->h2d), "h2d x");
+            ck(cudaEventRecord(h->ev_in[b], h->h2d), "record");
+        };
+        if (n > 0) load(0);
+        for (int i = 0; i < n; ++i) {
+            const int b = i & 1;
+            if (i + 1 < n) load(i + 1);          // enqueued before this solve blocks on its norms
+            ck(cudaStreamWaitEvent(h->stream, h->ev_in[b], 0), "wait");
+            if (!init_from_x) ck(cudaMemsetAsync(h->mx[b], 0, bytes, h->stream), "memset");
+            int rc = st_solve(h, h->mx[b], h->mf[b], tol, maxit, iters ? iters + i : nullptr,
+                              hist ? hist + (size_t)i * (maxit + 1) : nullptr);
+            if (rc) throw CudaError(g_err);
+            ck(cudaEventRecord(h->ev_done[b], h->stream), "record");
+            ck(cudaStreamWaitEvent(h->d2h, h->ev_done[b], 0), "wait");
+            ck(cudaMemcpyAsync(x_host[i], h->mx[b], bytes, cudaMemcpyDeviceToHost, h->d2h), "d2h x");
+            ck(cudaEventRecord(h->ev_out[b], h->d2h), "record");
+        }
+        ck(cudaStreamSynchronize(h->d2h), "sync");
+        ck(cudaStreamSynchronize(h->h2d), "sync");
     })
 }
 

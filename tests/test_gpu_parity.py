@@ -294,3 +294,24 @@ def test_constant_bank_slots_exhausted_falls_back(torch_cuda):
         assert np.array_equal(o, outs[0])
     for s in live:
         s.close()
+
+
+@pytest.mark.parametrize("init_from_x", [False, True])
+def test_solve_many_host_streaming(torch_cuda, init_from_x):
+    # st_solve_many_host: problems streamed through two device buffers and copy streams give the
+    # same results as one st_solve each (same kernels: bitwise)
+    torch = torch_cuda
+    w = workloads.small("c4")
+    s = solver(w)
+    rng = np.random.default_rng(61)
+    shape = (w.n_edges, w.q + 1, w.S)
+    fs = [torch.from_numpy(rng.uniform(-1, 1, shape)).pin_memory().numpy() for _ in range(5)]
+    x0 = [rng.uniform(-1, 1, shape) if init_from_x else np.zeros(shape) for _ in range(5)]
+    xs = [torch.from_numpy(a.copy()).pin_memory().numpy() for a in x0]
+    its, hists = s.solve_many_host(xs, fs, tol=1e-9, maxit=30, init_from_x=init_from_x)
+    for i in range(5):
+        x = torch.from_numpy(x0[i]).cuda()
+        it, h = s.solve(x, torch.from_numpy(fs[i]).cuda(), tol=1e-9, maxit=30)
+        assert its[i] == it and hists[i] == h
+        assert np.array_equal(xs[i], x.cpu().numpy())
+    assert s.solve_many_host([], [], tol=1e-9, maxit=3) == ([], [])
