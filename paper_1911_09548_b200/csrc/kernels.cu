@@ -176,49 +176,6 @@ __device__ __forceinline__ void stv(double *p, const double *v) {
     else p[0] = v[0];
 }
 
-// (M x)[a][j], (K x)[a][j] of row `row` at slabs k0+j.  WM/WK > 0: compile-time
-// ELL widths (full unroll: all gathers of a row in flight); 0: runtime width.
-template <int Q, int SPL, int WM, int WK>
-__device__ __forceinline__ void spatial_apply(const DevELL &M, const DevELL &K, int row, int k0, int S,
-                                              const double *__restrict__ x,
-                                              double (&mx)[Q][SPL], double (&kx)[Q][SPL]) {
-    const size_t QS = (size_t)Q * S;
-#pragma unroll
-    for (int a = 0; a < Q; ++a)
-#pragma unroll
-        for (int j = 0; j < SPL; ++j) { mx[a][j] = 0.0; kx[a][j] = 0.0; }
-    const Ent *eM = M.e + (size_t)row * (WM > 0 ? WM : M.width);
-    const int wm = WM > 0 ? WM : M.width;
-#pragma unroll (WM > 0 ? WM : 3)
-    for (int s = 0; s < wm; ++s) {
-        double v; int c;
-        ld_ent(eM + s, v, c);
-        const double *xc = x + (size_t)c * QS + k0;
-#pragma unroll
-        for (int a = 0; a < Q; ++a) {
-            double xv[SPL];
-            ldv<SPL>(xc + a * S, xv);
-#pragma unroll
-            for (int j = 0; j < SPL; ++j) mx[a][j] = fma(v, xv[j], mx[a][j]);
-        }
-    }
-    const Ent *eK = K.e + (size_t)row * (WK > 0 ? WK : K.width);
-    const int wk = WK > 0 ? WK : K.width;
-#pragma unroll (WK > 0 ? 11 : 3)
-    for (int s = 0; s < wk; ++s) {
-        double v; int c;
-        ld_ent(eK + s, v, c);
-        const double *xc = x + (size_t)c * QS + k0;
-#pragma unroll
-        for (int a = 0; a < Q; ++a) {
-            double xv[SPL];
-            ldv<SPL>(xc + a * S, xv);
-#pragma unroll
-            for (int j = 0; j < SPL; ++j) kx[a][j] = fma(v, xv[j], kx[a][j]);
-        }
-    }
-}
-
 // Merged M/K ELL: one column list, (M value, K value) pairs; one gather feeds both products.
 // Dictionary form (levels whose operator has at most kTabSize distinct (M, K) pairs, e.g.
 // uniform meshes with piecewise-constant coefficients): entry = col << 8 | value id, rows padded
