@@ -101,3 +101,31 @@ def test_fullsize_c5_converges(torch_cuda):
         del x
     print("c5 per-cycle rates", rates)
     assert rates["jacobi"] < 0.97 and rates["mg"] < 0.75 and rates["mg"] < rates["jacobi"]
+
+
+@pytest.mark.parametrize("name,inner", [("c4", "jacobi"), ("c5", "jacobi"), ("c4", "mg")])
+def test_fullsize_fixed_point(torch_cuda, name, inner):
+    # at the bench configuration: f = L x* (computed by the library's own residual with f = 0)
+    # makes x* a fixed point of the V-cycle -- every smoother, correction, transfer and the
+    # coarse solve must map a zero residual to a zero update (up to rounding)
+    torch = torch_cuda
+    import paper_1911_09548_b200 as p
+    w = {"c4": lambda: workloads.c4(), "c5": lambda: workloads.c5()}[name]()
+    s = p.Solver.from_workload(w, inner=inner)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(17)
+    xs = torch.empty(s.shape, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g)
+    zero = torch.zeros_like(xs)
+    f = torch.empty_like(xs)
+    s.residual(xs, zero, f)                 # f = 0 - L x*
+    f.neg_()
+    x = xs.clone()
+    s.vcycle(x, f)
+    torch.cuda.synchronize()
+    rel = float(torch.linalg.vector_norm(x - xs) / torch.linalg.vector_norm(xs))
+    print(name, inner, "|V(x*, L x*) - x*| / |x*| =", rel)
+    # rounding of f - L x* (~1e-16 relative) is amplified by the coarse corrections: c5's
+    # coefficient contrast 1e5 gives a one-ulp sensitivity of ~1e-12 per cycle at 6^3 (DESIGN.md
+    # R12), growing like h^-2 to ~6e-11 at 48^3
+    assert rel <= (1e-12 if name == "c4" else 1e-9)
+    s.close()
