@@ -204,7 +204,8 @@ double nvec(const DevLevel &L, int Q) { return 8.0 * L.n_nodes * Q * L.S; }
 
 // prev: end values (time node q) of the slab before this level's first slab (the previous
 // rank's last slab), or null for the zero initial state (PAPER.md l.47-48 homogeneous u^0)
-// One inner spatial V-cycle (R13) for A_k z = r on all slabs at once (the slabs are
+// One inner spatial V-cycle (R13: the "A_k^{-1} sufficiently well approximated" of
+// Eq. (2)) for A_k z = r on all slabs at once (the slabs are
 // independent: no time coupling below the outer residual).  V[j] shares the chain operators
 // and its own vectors; returns the buffer holding z.  j = 0 enters with the first edge sweep
 // from zero already done (fused into the outer residual) and, with xout set, its last edge

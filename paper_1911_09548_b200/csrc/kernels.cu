@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kBlock) k_axpy(size_t n, double alpha, const d
 
 // ------------------------------------------------- two-pass nodal residual
 // Pass 1 (edge rows): u = f - (Ct (x) M) x + (Nt (x) M) x_prev, the residual without K
-// (G^T K = 0, so G^T u = G^T (f - L x)).  Pays off where M is narrow (9 slots on uniform
+// (G^T K = 0, so G^T u = G^T (f - L x): the G^T (f - L x) of Eq. (5)).  Pays off where M is narrow (9 slots on uniform
 // hexes against 54 for the node-row G^T M of k_gtr): fewer L1 gathers for one more vector pass.
 template <int Q, int SPL, int WM>
 __global__ void __launch_bounds__(kBlock, 4) k_res_mass(BoxMap m, DevELL M, const double *__restrict__ x,
@@ -976,7 +976,8 @@ __global__ void __launch_bounds__(32 * kMarchWarps, 3) k_sweep_march(MarchMap mm
 // ------------------------------------------------------------- transfers
 // Restriction: fc[rc][a][K] = sum_{(rf,w) in R_s row rc} w * sum_{j,b} Pt_K[(j Q + b)][a] r[rf][b][2K+j]
 // one thread per (coarse row, coarse slab K); the fine slab pair (2K, 2K+1) is one 16-byte load.
-// space-only restriction / prolongation of the inner spatial V-cycle (R13): same slabs
+// space-only restriction / prolongation of the inner spatial V-cycle (R13, the
+// approximation of A_k^{-1} in Eq. (2)): same slabs
 template <int Q, bool PROLONG>
 __global__ void __launch_bounds__(kBlock) k_space_transfer(Map m, DevELL T, const double *__restrict__ in,
                                                            double *__restrict__ out) {
