@@ -65,3 +65,12 @@ def test_edge_case_vcycle(label, kw, opts):
         # a single level is the exact forward substitution: the residual vanishes
         rn, fn = s.residual(x, f, norms=True)
         assert rn <= 1e-12 * fn
+
+
+def test_too_many_slabs_for_one_gpu_is_refused():
+    # the row kernels index a level's (edge, slab) pairs with 32-bit integers: 64^3 edges x 4096
+    # slabs (3.3e9) is refused with st_setup's "unsupported" code instead of overflowing
+    import paper_1911_09548_b200 as p
+    w = workloads.c4(n=64, S=4096)
+    with pytest.raises(p.StError, match="libst error 3"):
+        p.Solver.from_workload(w)
