@@ -1208,11 +1208,13 @@ static inline BoxMap node_map(const DevLevel &L) { return make_boxmap(L.S, L.sch
     }
 #define ST_DISPATCH_SPL(spl, ...)                               \
     if (spl == 2) { constexpr int SP = 2; __VA_ARGS__; }        \
-    else { constexpr int SP = 1; __VA_ARGS__; }
+    else if (spl == 1) { constexpr int SP = 1; __VA_ARGS__; }   \
+    else throw std::logic_error("slabs per lane not instantiated for this kernel");
 #define ST_DISPATCH_SPL4(spl, ...)                              \
     if (spl == 4) { constexpr int SP = 4; __VA_ARGS__; }        \
     else if (spl == 2) { constexpr int SP = 2; __VA_ARGS__; }   \
-    else { constexpr int SP = 1; __VA_ARGS__; }
+    else if (spl == 1) { constexpr int SP = 1; __VA_ARGS__; }   \
+    else throw std::logic_error("slabs per lane not instantiated for this kernel");
 // compile-time ELL widths of the common stencils: uniform hexes (9, 33), general hexes
 // (33, 33), uniform quads (3, 7), general quads (7, 7); anything else runtime
 #define ST_DISPATCH_W(wm, wk, ...)                                                        \
@@ -1322,8 +1324,10 @@ void launch_gtr(Stream st, const DevLevel &L, const KT &kt, int Q, const double 
 
 void launch_res_mass(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
                      const double *prev, double *u) {
-    const BoxMap m = edge_map(L);
-    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, {
+    // 4 slabs per lane: measured 68 vs 75 ms per 5 c4 V-cycles at 2 (env ST_RESMASS_SPL)
+    static const int spl = std::getenv("ST_RESMASS_SPL") ? std::atoi(std::getenv("ST_RESMASS_SPL")) : 4;
+    const BoxMap m = edge_map(L, spl);
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL4(m.spl, {
         if (L.M.width == 9) k_res_mass<QQ, SP, 9><<<grid(m), kBlock, 0, st>>>(m, L.M, x, f, prev, u, kt);
         else if (L.M.width == 3) k_res_mass<QQ, SP, 3><<<grid(m), kBlock, 0, st>>>(m, L.M, x, f, prev, u, kt);
         else k_res_mass<QQ, SP, 0><<<grid(m), kBlock, 0, st>>>(m, L.M, x, f, prev, u, kt);
