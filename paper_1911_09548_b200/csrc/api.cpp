@@ -761,13 +761,17 @@ int st_solve_many_host(st_handle *h, int n, double *const *x_host, const double 
             ck(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking), "stream");
             ck(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking), "stream");
         }
-        // buffer b is free for problem i once problem i-2's solve and D2H copy are done
+        // f buffer b is free for problem i once problem i-2's solve is done; x buffer b once
+        // problem i-2's D2H copy is done too (only the x copy / the zeroing waits for that, so
+        // the H2D of f never queues behind the previous D2H)
         auto load = [&](int i) {
             const int b = i & 1;
             ck(cudaStreamWaitEvent(h->h2d, h->ev_done[b], 0), "wait");
-            ck(cudaStreamWaitEvent(h->h2d, h->ev_out[b], 0), "wait");
             ck(cudaMemcpyAsync(h->mf[b], f_host[i], bytes, cudaMemcpyHostToDevice, h->h2d), "h2d f");
-            if (init_from_x) ck(cudaMemcpyAsync(h->mx[b], x_host[i], bytes, cudaMemcpyHostToDevice, h->h2d), "h2d x");
+            if (init_from_x) {
+                ck(cudaStreamWaitEvent(h->h2d, h->ev_out[b], 0), "wait");
+                ck(cudaMemcpyAsync(h->mx[b], x_host[i], bytes, cudaMemcpyHostToDevice, h->h2d), "h2d x");
+            }
             ck(cudaEventRecord(h->ev_in[b], h->h2d), "record");
         };
         if (n > 0) load(0);
@@ -775,6 +779,7 @@ int st_solve_many_host(st_handle *h, int n, double *const *x_host, const double 
             const int b = i & 1;
             if (i + 1 < n) load(i + 1);          // enqueued before this solve blocks on its norms
             ck(cudaStreamWaitEvent(h->stream, h->ev_in[b], 0), "wait");
+            ck(cudaStreamWaitEvent(h->stream, h->ev_out[b], 0), "wait");
             if (!init_from_x) ck(cudaMemsetAsync(h->mx[b], 0, bytes, h->stream), "memset");
             int rc = st_solve(h, h->mx[b], h->mf[b], tol, maxit, iters ? iters + i : nullptr,
                               hist ? hist + (size_t)i * (maxit + 1) : nullptr);
