@@ -104,3 +104,20 @@ def test_distributed_solve_history():
     Xd, hd, _ = run(2, "c1", 1, {}, maxit=6)
     Xr, hr = reference("c1", 1, {}, 6)
     np.testing.assert_allclose(hd, hr, rtol=1e-10, atol=1e-14)
+
+
+def test_bench_reference_arm_json_line():
+    # bench.py --impl reference times the CPU oracle (the reference arm for this tier) and prints
+    # one JSON line with the contract's keys; runs without a GPU
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "dtype", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0

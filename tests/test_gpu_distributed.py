@@ -106,3 +106,22 @@ def test_two_ranks_one_gpu(name, P, opts):
     x.zero_()
     it, h1 = s.solve(x, f, tol=1e-10, maxit=5)
     np.testing.assert_allclose(hist, h1, rtol=1e-10, atol=1e-14)
+
+
+def test_bench_two_ranks_one_gpu_gloo():
+    # the N > 1 path of bench.py (DistributedVCycle timing, max over ranks, e2e) with two ranks on
+    # one GPU: gloo instead of NCCL (ST_BENCH_BACKEND); rank 0 prints the JSON line
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ST_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--slabs", "16", "--cells", "8", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0 and d["e2e"]["value"] > 0
