@@ -190,6 +190,10 @@ struct MKELL {
 };
 
 constexpr int kTabSize = 256, kTabSlots = 14;
+#ifndef ST_DICT_UNROLL
+#define ST_DICT_UNROLL 9
+#endif
+constexpr int kDictUnroll = ST_DICT_UNROLL;   // batches of 4 dictionary entries unrolled
 #ifndef ST_SWEEP_MINB
 #define ST_SWEEP_MINB 3
 #endif
@@ -223,7 +227,7 @@ __device__ __forceinline__ void spatial_apply_mk(const MKELL &A, int row, int k0
         static_assert(!DICT || W > 0, "dictionary ELL needs a compile-time width");
         constexpr int W4 = (W + 3) / 4 * 4;
         const uint4 *pp = reinterpret_cast<const uint4 *>(A.pk + (size_t)row * W4);
-#pragma unroll
+#pragma unroll (kDictUnroll)
         for (int s0 = 0; s0 < W; s0 += 4) {
             const uint4 e4 = __ldg(pp + s0 / 4);
             const unsigned es[4] = {e4.x, e4.y, e4.z, e4.w};
