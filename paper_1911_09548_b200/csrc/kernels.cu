@@ -289,7 +289,7 @@ __device__ __forceinline__ void coupling(const DevELL &M, int row, int k0, int S
 // r = f - L x; optionally z = omega_s D^{-1} r (first Jacobi sweep of B from zero)
 // and per-block partial sums of |r|^2.
 template <int Q, int SPL, int WM, int WK, bool R_OUT, bool Z_OUT, bool NORM, bool COUPLE = true, bool DICT = false>
-__global__ void __launch_bounds__(kBlock, DICT ? 4 : 1) k_residual(BoxMap m, DevELL M, MKELL MK, const double *__restrict__ tau,
+__global__ void __launch_bounds__(kBlock, DICT ? 4 : 0) k_residual(BoxMap m, DevELL M, MKELL MK, const double *__restrict__ tau,
                                                      const double *__restrict__ x, const double *__restrict__ f,
                                                      const double *__restrict__ prev, double *__restrict__ r,
                                                      double *__restrict__ z, const double *__restrict__ dM,
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kBlock, DICT ? 4 : 1) k_residual(BoxMap m, Dev
 // LAST: x += omega * znew (the smoother update of Eq. 2), in place (x is only
 // read at its own row).
 template <int Q, int SPL, int WM, int WK, bool LAST, bool RECON, bool DICT = false>
-__global__ void __launch_bounds__(kBlock, DICT ? ST_SWEEP_MINB : 1) k_sweep(BoxMap m, DevELL M, MKELL MK, const double *__restrict__ tau,
+__global__ void __launch_bounds__(kBlock, DICT ? ST_SWEEP_MINB : 0) k_sweep(BoxMap m, DevELL M, MKELL MK, const double *__restrict__ tau,
                                                   const double *__restrict__ dM, const double *__restrict__ dK,
                                                   const double *__restrict__ z, const double *__restrict__ r,
                                                   double *out, double omega_s, double omega, KT kt) {
