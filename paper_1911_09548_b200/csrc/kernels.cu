@@ -214,10 +214,12 @@ __device__ __forceinline__ void mk_fma(const double2 v, const double *__restrict
     }
 }
 
-template <int Q, int SPL, int W, bool DICT = false>
+template <int Q, int SPL, int W, bool DICT = false, bool FOLD = false>
 __device__ __forceinline__ void spatial_apply_mk(const MKELL &A, int row, int k0, int S,
                                                  const double *__restrict__ x,
-                                                 double (&mx)[Q][SPL], double (&kx)[Q][SPL]) {
+                                                 double (&mx)[Q][SPL], double (&kx)[Q][SPL],
+                                                 const double *cp = nullptr, bool cp_prev = false,
+                                                 double *mp0 = nullptr) {
     const size_t QS = (size_t)Q * S;
 #pragma unroll
     for (int a = 0; a < Q; ++a)
@@ -248,6 +250,10 @@ __device__ __forceinline__ void spatial_apply_mk(const MKELL &A, int row, int k0
         const int c = __ldg(cc + s);
         const double2 v = __ldg(vv + s);
         mk_fma<Q, SPL>(v, x + (size_t)c * QS + k0, S, mx, kx);
+        // FOLD (M and K share one 33-slot pattern, e.g. jittered hexes): the first lane of a row
+        // group also gathers x_q of the slab before its chunk for the upwind coupling here, so
+        // its 33 loads overlap the merged gathers instead of forming a serial tail
+        if (FOLD && cp) *mp0 = fma(v.x, __ldg(cp + (cp_prev ? (size_t)c : (size_t)c * QS)), *mp0);
     }
 }
 
@@ -299,11 +305,24 @@ __global__ void __launch_bounds__(kBlock, DICT ? 4 : 0) k_residual(BoxMap m, Dev
     box_loop(m, [&](int row, int k0, bool valid) {
         const int S = m.S;
         double mx[Q][SPL], kx[Q][SPL], mp[SPL];
-        spatial_apply_mk<Q, SPL, WK, DICT>(MK, row, k0, S, x, mx, kx);
-        if (COUPLE) coupling<Q, SPL, WM>(M, row, k0, S, 1 << m.lpr_log2, x, prev, mx, mp);
-        else
+        constexpr bool FOLD = !DICT && COUPLE && WM == 33 && WK == 33;
+        if (FOLD) {
+            const int lpr = 1 << m.lpr_log2;
+            const bool first = ((threadIdx.x & 31) & (lpr - 1)) == 0;
+            const double *cp = !first ? nullptr : k0 > 0 ? x + (size_t)(Q - 1) * S + k0 - 1 : prev;
+            double mp0 = 0.0;
+            spatial_apply_mk<Q, SPL, WK, false, true>(MK, row, k0, S, x, mx, kx, cp, k0 == 0, &mp0);
 #pragma unroll
-            for (int j = 0; j < SPL; ++j) mp[j] = 0.0;
+            for (int j = 1; j < SPL; ++j) mp[j] = mx[Q - 1][j - 1];
+            const double up = __shfl_up_sync(0xffffffffu, mx[Q - 1][SPL - 1], 1, lpr);
+            mp[0] = first ? mp0 : up;
+        } else {
+            spatial_apply_mk<Q, SPL, WK, DICT>(MK, row, k0, S, x, mx, kx);
+            if (COUPLE) coupling<Q, SPL, WM>(M, row, k0, S, 1 << m.lpr_log2, x, prev, mx, mp);
+            else
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) mp[j] = 0.0;
+        }
         if (!valid) return;
         double t[SPL];
         ldv<SPL>(tau + k0, t);
@@ -531,6 +550,12 @@ __global__ void __launch_bounds__(kBlock) k_gtr(BoxMap m, DevELL GT, DevELL GtM,
         for (int a = 0; a < Q; ++a)
 #pragma unroll
             for (int j = 0; j < SPL; ++j) gm[a][j] = 0.0;
+        // coupling: (G^T M x_q) at slab k-1 comes from the previous lane of the row group; the
+        // first lane gathers it inside the G^T M loop (its loads overlap the main gathers)
+        const int lpr = 1 << m.lpr_log2;
+        const bool first = ((threadIdx.x & 31) & (lpr - 1)) == 0;
+        const double *cp = !(COUPLE && first) ? nullptr : k0 > 0 ? x + (size_t)(Q - 1) * S + k0 - 1 : prev;
+        double acc0 = 0.0;
         const Ent *e = GtM.e + (size_t)node * GtM.width;
 #pragma unroll 6
         for (int s = 0; s < GtM.width; ++s) {
@@ -544,27 +569,13 @@ __global__ void __launch_bounds__(kBlock) k_gtr(BoxMap m, DevELL GT, DevELL GtM,
 #pragma unroll
                 for (int j = 0; j < SPL; ++j) gm[a][j] = fma(v, xv[j], gm[a][j]);
             }
+            if (cp) acc0 = fma(v, __ldg(cp + (k0 > 0 ? (size_t)c * QS : (size_t)c)), acc0);
         }
-        // coupling: (G^T M x_q) at slab k-1, from the previous lane of the row group or explicit
-        const int lpr = 1 << m.lpr_log2;
         double mp[SPL];
 #pragma unroll
         for (int j = 1; j < SPL; ++j) mp[j] = COUPLE ? gm[Q - 1][j - 1] : 0.0;
         const double up = __shfl_up_sync(0xffffffffu, gm[Q - 1][SPL - 1], 1, lpr);
-        if (!COUPLE) {
-            mp[0] = 0.0;
-        } else if (((threadIdx.x & 31) & (lpr - 1)) != 0) {
-            mp[0] = up;
-        } else {
-            double acc = 0.0;
-            for (int s = 0; s < GtM.width; ++s) {
-                double v; int c;
-                ld_ent(e + s, v, c);
-                const double xp = k0 > 0 ? __ldg(x + (size_t)c * QS + (Q - 1) * S + k0 - 1) : (prev ? __ldg(prev + c) : 0.0);
-                acc = fma(v, xp, acc);
-            }
-            mp[0] = acc;
-        }
+        mp[0] = !COUPLE ? 0.0 : first ? acc0 : up;
         if (!valid) return;
         double gf[Q][SPL];
 #pragma unroll
