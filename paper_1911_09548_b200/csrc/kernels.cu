@@ -1312,7 +1312,8 @@ void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, 
     // Env ST_SWEEP_DICT=0 forces the plain form (measurements).
     static const bool no_dict = std::getenv("ST_SWEEP_DICT") && std::getenv("ST_SWEEP_DICT")[0] == '0';
     const bool dict = L.mk_pk && !no_dict;
-    const BoxMap m = edge_map(L, dict ? 2 : 4);
+    static const int plain_spl = std::getenv("ST_SWEEP_PLAIN_SPL") ? std::atoi(std::getenv("ST_SWEEP_PLAIN_SPL")) : 4;
+    const BoxMap m = edge_map(L, dict ? 2 : plain_spl);
     const int g = grid(m);
     const MKELL MK{L.mk_col, L.mk_val, L.mk_width, dict ? L.mk_pk : nullptr, L.mk_tab};
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL4(m.spl, ST_DISPATCH_W(L.M.width, L.mk_width, {
