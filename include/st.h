@@ -24,7 +24,9 @@
  *   vector (right-hand side of L x = f); the initial state is zero.
  *
  * Memory: every pointer argument documented "device" must be a CUDA device
- * pointer on the device that was current at st_setup; "host" pointers are
+ * pointer on the device that was current at st_setup, and space-time vectors
+ * (x, f, r, fc, xc) must be 16-byte aligned (the kernels move slab pairs as
+ * 16-byte vectors; a misaligned vector is refused with code 1); "host" pointers are
  * ordinary (pageable or pinned) host memory.  The library never takes
  * ownership of caller memory; it owns everything it allocates in st_setup and
  * frees it in st_free.  All device work is enqueued on the handle's stream

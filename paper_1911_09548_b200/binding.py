@@ -230,6 +230,8 @@ class Solver:
         import torch
         if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
             raise StError("expected a contiguous float64 CUDA tensor")
+        if t.data_ptr() % 16:
+            raise StError("expected a 16-byte aligned tensor (the kernels use 16-byte vector loads)")
         return ctypes.c_void_p(t.data_ptr())
 
     def residual(self, x, f, r=None, norms=False):

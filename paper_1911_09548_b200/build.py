@@ -1,4 +1,5 @@
 """Build libst.so (sm_100a) in-tree with nvcc.  Called by __graft_entry__.build()."""
+import glob
 import os
 import subprocess
 import sys
@@ -13,7 +14,8 @@ FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-li
 
 def build(verbose=False, extra=()):
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "internal.h"), os.path.join(HERE, "..", "include", "st.h")]
+    # every source and header under csrc/ (kernels.cu includes march.cuh, stencil.cuh, ...)
+    deps = sorted(glob.glob(os.path.join(CSRC, "*"))) + [os.path.join(HERE, "..", "include", "st.h")]
     if os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps) and not extra:
         return LIB
     cmd = ["nvcc", *FLAGS, *extra, "-o", LIB, *srcs, "-lcudart"]

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <initializer_list>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -174,6 +176,11 @@ struct st_handle {
         D.mk_tab = off;
     }
     ~st_handle() {
+        // drain every stream that may still run this handle's kernels or copies before the
+        // constant-bank dictionary slots and device buffers are released for reuse
+        if (stream) cudaStreamSynchronize(stream);
+        if (h2d) cudaStreamSynchronize(h2d);
+        if (d2h) cudaStreamSynchronize(d2h);
         clear_graphs();
         for (int b = 0; b < 2; ++b)
             for (cudaEvent_t e : {ev_in[b], ev_done[b], ev_out[b]})
@@ -442,6 +449,16 @@ int fail(int code, const std::string &msg) {
     return code;
 }
 
+// the kernels move slab pairs / quadruples as 16-byte vectors: device vector arguments must be
+// 16-byte aligned (a view at an odd element offset would fault and kill the CUDA context)
+bool misaligned(std::initializer_list<const void *> ptrs) {
+    for (const void *p : ptrs)
+        if (p && (reinterpret_cast<uintptr_t>(p) & 15u)) return true;
+    return false;
+}
+#define ST_CHECK_ALIGNED(...) \
+    if (misaligned({__VA_ARGS__})) return fail(1, "device vectors must be 16-byte aligned")
+
 #define ST_GUARD(body)                                              \
     try {                                                           \
         body;                                                       \
@@ -664,6 +681,7 @@ int st_setup(const st_params *p, st_handle **out) {
 
 int st_free(st_handle *h) {
     if (!h) return 0;
+    if (h->stream) cudaStreamSynchronize(h->stream);   // the user's stream too
     if (h->stream && h->own_stream) cudaStreamDestroy(h->stream);
     h->stream = nullptr;
     delete h;
@@ -680,6 +698,7 @@ int st_set_stream(st_handle *h, void *stream) {
 
 int st_residual(st_handle *h, const double *x, const double *f, double *r, double *norms) {
     if (!h || !x || !f) return fail(1, "null argument");
+    ST_CHECK_ALIGNED(x, f, r);
     ST_GUARD({
         DevLevel &L = h->dl[0];
         auto s = (st::Stream)h->stream;
@@ -696,6 +715,7 @@ int st_residual(st_handle *h, const double *x, const double *f, double *r, doubl
 
 int st_vcycle(st_handle *h, double *x, const double *f) {
     if (!h || !x || !f) return fail(1, "null argument");
+    ST_CHECK_ALIGNED(x, f);
     if (h->nranks > 1) return fail(1, "multi-rank handles run the V-cycle through the st_lv_* level operations");
     ST_GUARD(run_vcycle(h, x, f))
 }
@@ -712,6 +732,7 @@ int st_set_graphs(st_handle *h, int enable) {
 
 int st_solve(st_handle *h, double *x, const double *f, double tol, int maxit, int *iters, double *hist) {
     if (!h || !x || !f || maxit < 0) return fail(1, "bad argument");
+    ST_CHECK_ALIGNED(x, f);
     if (h->nranks > 1) return fail(1, "multi-rank handles solve through paper_1911_09548_b200.distributed");
     ST_GUARD({
         const double nf = std::sqrt(norm2_plain(h, f, vec_len(h->dl[0], h->Q)));
@@ -918,6 +939,7 @@ int st_lv_get(const st_handle *hc, int set, int level, st_level_t *out) {
 int st_lv_residual(st_handle *h, int set, int level, const double *x, const double *f, const double *prev, double *r,
                    double *norm2) {
     if (!h || !x || !f) return fail(1, "null argument");
+    ST_CHECK_ALIGNED(x, f, r);
     ST_GUARD({
         DevLevel &L = level_of(h, set, level);
         auto s = (st::Stream)h->stream;
@@ -936,21 +958,25 @@ int st_lv_residual(st_handle *h, int set, int level, const double *x, const doub
 
 int st_lv_smooth_S(st_handle *h, int set, int level, double *x, const double *f, const double *prev) {
     if (!h || !x || !f) return fail(1, "null argument");
+    ST_CHECK_ALIGNED(x, f);
     ST_GUARD(smooth_S(h, level_of(h, set, level), x, f, prev))
 }
 
 int st_lv_correct_local(st_handle *h, int set, int level, double *x, const double *f, const double *prev, double *tot) {
     if (!h || !x || !f) return fail(1, "null argument");
+    ST_CHECK_ALIGNED(x, f);
     ST_GUARD(correct_A_local(h, level_of(h, set, level), x, f, prev, tot))
 }
 
 int st_lv_correct_apply(st_handle *h, int set, int level, double *x, const double *carry) {
     if (!h || !x) return fail(1, "null argument");
+    ST_CHECK_ALIGNED(x);
     ST_GUARD(correct_A_apply(h, level_of(h, set, level), x, carry))
 }
 
 int st_lv_restrict(st_handle *h, int set, int level, const double *r, double *fc) {
     if (!h || !r || !fc) return fail(1, "null argument");
+    ST_CHECK_ALIGNED(r, fc);
     ST_GUARD({
         auto &V = level_set(h, set);
         if (level < 0 || level + 1 >= (int)V.size()) throw std::invalid_argument("no coarser level in this set");
@@ -960,6 +986,7 @@ int st_lv_restrict(st_handle *h, int set, int level, const double *r, double *fc
 
 int st_lv_prolong(st_handle *h, int set, int level, const double *xc, double *x) {
     if (!h || !xc || !x) return fail(1, "null argument");
+    ST_CHECK_ALIGNED(xc, x);
     ST_GUARD({
         auto &V = level_set(h, set);
         if (level < 0 || level + 1 >= (int)V.size()) throw std::invalid_argument("no coarser level in this set");
@@ -969,6 +996,7 @@ int st_lv_prolong(st_handle *h, int set, int level, const double *xc, double *x)
 
 int st_lv_vcycle(st_handle *h, int set, int level, double *x, const double *f) {
     if (!h || !x || !f) return fail(1, "null argument");
+    ST_CHECK_ALIGNED(x, f);
     ST_GUARD({
         auto &V = level_set(h, set);
         if (V.back().Ainv == nullptr) throw std::invalid_argument("this level set has no coarsest level");
