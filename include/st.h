@@ -208,6 +208,14 @@ int st_plan(const st_params *p, st_info_t *info);
  * rows*width entries.  For checking the setup against an independent
  * assembly. */
 int st_host_matrix(const st_params *p, int level, int which, int *rows, int *width, int *col, double *val);
+
+/* Diagnostics: bit i of *mask (host) is set when the kernel variant st_variant_name(i) (e.g.
+ * "sweep/spl4": the block-Jacobi sweep at 4 slabs per lane; "node_scan/multichunk": the Sigma_t
+ * scan carrying over several slab chunks) has been launched by this process since the last
+ * reset; reset != 0 clears the log after reading.  Lets tests prove which code paths ran.
+ * st_variant_name returns NULL past the last variant. */
+int st_kernel_variants(uint64_t *mask, int reset);
+const char *st_variant_name(int bit);
 const char *st_last_error(void);
 
 #ifdef __cplusplus

@@ -96,7 +96,7 @@ def restrict(H, l, R):
     q = H.q
     th = H.theta(l)
     S, Q, n = R.shape
-    Fc = np.zeros((S // 2, Q, n))
+    Fc = np.zeros((S // 2, Q, n), dtype=R.dtype)
     for K in range(S // 2):
         Pt = time_dg.prolongation(q, th[K])                  # (2Q, Q)
         pair = R[2 * K:2 * K + 2].reshape(2 * Q, n)
@@ -115,7 +115,7 @@ def prolongate(H, l, Xc):
         Xc = H.levels[l].spatial(Pe, Xc)
     th = H.theta(l)
     Sc, Q, n = Xc.shape
-    X = np.zeros((2 * Sc, Q, n))
+    X = np.zeros((2 * Sc, Q, n), dtype=Xc.dtype)
     for K in range(Sc):
         Pt = time_dg.prolongation(q, th[K])
         X[2 * K:2 * K + 2] = (Pt @ Xc[K]).reshape(2, Q, n)

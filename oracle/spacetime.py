@@ -82,16 +82,61 @@ def residual(lv, X, F):
     return F - apply_L(lv, X)
 
 
+def inv_blocks(D):
+    """Inverse of every (Q x Q) block of D (shape (..., Q, Q)) in D's precision.  float64 uses
+    LAPACK (np.linalg.inv); other dtypes (np.longdouble for the extended-precision reference of
+    the c3 tolerance, R12) Gauss-Jordan elimination with partial pivoting."""
+    if D.dtype == np.float64:
+        return np.linalg.inv(D)
+    A = np.array(D, copy=True)
+    Q = A.shape[-1]
+    B = np.broadcast_to(np.eye(Q, dtype=A.dtype), A.shape).copy()
+    for c in range(Q):
+        piv = np.argmax(np.abs(A[..., c:, c]), axis=-1) + c
+        idx = np.indices(piv.shape)
+        rows_c = A[..., c, :].copy(); rows_p = A[(*idx, piv)].copy()
+        A[..., c, :] = rows_p; A[(*idx, piv)] = rows_c
+        rows_c = B[..., c, :].copy(); rows_p = B[(*idx, piv)].copy()
+        B[..., c, :] = rows_p; B[(*idx, piv)] = rows_c
+        p = A[..., c, c][..., None].copy()
+        A[..., c, :] /= p; B[..., c, :] /= p
+        for r in range(Q):
+            if r != c:
+                fct = A[..., r, c][..., None].copy()
+                A[..., r, :] -= fct * A[..., c, :]
+                B[..., r, :] -= fct * B[..., c, :]
+    return B
+
+
+def dense_solve(A, b):
+    """x = A^{-1} b by Gaussian elimination with partial pivoting in A's precision (used for the
+    extended-precision coarsest forward substitution)."""
+    A = np.array(A, copy=True); b = np.array(b, copy=True)
+    n = A.shape[0]
+    for c in range(n):
+        p = c + int(np.argmax(np.abs(A[c:, c])))
+        if p != c:
+            A[[c, p]] = A[[p, c]]; b[[c, p]] = b[[p, c]]
+        f = A[c + 1:, c] / A[c, c]
+        A[c + 1:, c:] -= np.outer(f, A[c, c:])
+        b[c + 1:] -= f * b[c]
+    x = np.zeros_like(b)
+    for c in range(n - 1, -1, -1):
+        x[c] = (b[c] - A[c, c + 1:] @ x[c + 1:]) / A[c, c]
+    return x
+
+
 def block_jacobi_inverse(lv, k, R, nu_s, omega_s):
     """nu_s damped block-Jacobi sweeps on A_k z = R_k from z = 0.
 
     The Jacobi block of edge e is the (q+1)x(q+1) matrix
     D_e = Ct M_ee + tau_k Mt K_ee (all time nodes of one edge)."""
     Q = lv.q + 1
-    dM = lv.M.diagonal(); dK = lv.K.diagonal()
-    D = lv.Ct[None] * dM[:, None, None] + lv.tau[k] * lv.Mt[None] * dK[:, None, None]   # (n, Q, Q)
-    Dinv = np.linalg.inv(D)
-    z = np.zeros((Q, lv.n))
+    dt = R.dtype                    # float64, or np.longdouble for the extended-precision reference
+    dM = lv.M.diagonal().astype(dt); dK = lv.K.diagonal().astype(dt)
+    D = lv.Ct.astype(dt)[None] * dM[:, None, None] + dt.type(lv.tau[k]) * lv.Mt.astype(dt)[None] * dK[:, None, None]   # (n, Q, Q)
+    Dinv = inv_blocks(D)
+    z = np.zeros((Q, lv.n), dtype=dt)
     for _ in range(nu_s):
         Az = lv.Ct @ (lv.M @ z.T).T + lv.tau[k] * (lv.Mt @ (lv.K @ z.T).T)
         d = R - Az
@@ -202,8 +247,8 @@ def sigma_t(lv, Z):
     G^T L G = L_t (x) K_n, i.e. forward substitution of the pure dG(q) ODE
     u' = z:  Y_k = Ct^{-1} (Z_k + Nt Y_{k-1})."""
     Y = np.zeros_like(Z)
-    Ctinv = np.linalg.inv(lv.Ct)
-    prev = np.zeros(Z.shape[1:])
+    Ctinv = inv_blocks(lv.Ct.astype(Z.dtype))
+    prev = np.zeros(Z.shape[1:], dtype=Z.dtype)
     for k in range(Z.shape[0]):
         Y[k] = Ctinv @ (Z[k] + lv.Nt @ prev)
         prev = Y[k]
@@ -237,9 +282,13 @@ def hybrid_smooth(lv, X, F, opts, phase):
 def forward_solve(lv, F, prev=None):
     """Exact forward substitution in time: X_k = A_k^{-1} (F_k + Nt M X_{k-1})."""
     X = np.zeros_like(F)
-    p = np.zeros((lv.q + 1, lv.n)) if prev is None else prev
+    p = np.zeros((lv.q + 1, lv.n), dtype=F.dtype) if prev is None else prev
     for k in range(lv.S):
         rhs = F[k] + lv.Nt @ (lv.M @ p.T).T
-        X[k] = lv.Ainv_exact(k).solve(rhs.reshape(-1)).reshape(lv.q + 1, lv.n)
+        if F.dtype == np.float64:
+            X[k] = lv.Ainv_exact(k).solve(rhs.reshape(-1)).reshape(lv.q + 1, lv.n)
+        else:       # extended-precision reference: dense elimination in F's precision
+            A = lv.A_k(k).toarray().astype(F.dtype)
+            X[k] = dense_solve(A, rhs.reshape(-1)).reshape(lv.q + 1, lv.n)
         p = X[k]
     return X

@@ -19,7 +19,7 @@ LEVEL_OPS = ["st_lv_count", "st_lv_get", "st_lv_residual", "st_lv_smooth_S", "st
              "st_copy_slabs", "st_zero", "st_sync"]
 EXPORTED = ["st_setup", "st_free", "st_set_stream", "st_residual", "st_vcycle", "st_set_graphs", "st_solve",
             "st_solve_host", "st_solve_many_host", "st_info", "st_profile", "st_profile_read", "st_plan", "st_host_matrix",
-            *LEVEL_OPS, "st_last_error"]
+            *LEVEL_OPS, "st_kernel_variants", "st_variant_name", "st_last_error"]
 
 
 class StParams(ctypes.Structure):
@@ -97,8 +97,11 @@ def load():
     lib.st_copy_slabs.argtypes = [vp, ci, ci, ci, vp, ci, ci, vp, ci, ci, ci]
     lib.st_zero.argtypes = [vp, vp, i64]
     lib.st_sync.argtypes = [vp]
+    lib.st_kernel_variants.argtypes = [ctypes.POINTER(ctypes.c_uint64), ci]
+    lib.st_variant_name.argtypes = [ci]
+    lib.st_variant_name.restype = ctypes.c_char_p
     lib.st_last_error.restype = ctypes.c_char_p
-    for name in EXPORTED[:-1]:
+    for name in EXPORTED[:-3] + ["st_kernel_variants"]:
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -106,6 +109,21 @@ def load():
 
 class StError(RuntimeError):
     pass
+
+
+def kernel_variants(reset=False):
+    """Names of the kernel variants launched by this process (st_kernel_variants)."""
+    lib = load()
+    mask = ctypes.c_uint64()
+    _check(lib.st_kernel_variants(ctypes.byref(mask), 1 if reset else 0))
+    out, i = set(), 0
+    while True:
+        name = lib.st_variant_name(i)
+        if name is None:
+            return out
+        if mask.value >> i & 1:
+            out.add(name.decode())
+        i += 1
 
 
 def _check(rc):

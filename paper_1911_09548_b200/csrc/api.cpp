@@ -515,6 +515,14 @@ static void parse_options(const st_params *p, st::Options &o) {
 
 const char *st_last_error(void) { return g_err.c_str(); }
 
+int st_kernel_variants(uint64_t *mask, int reset) {
+    if (!mask) return fail(1, "null argument");
+    *mask = (uint64_t)st::variants(reset != 0);
+    return 0;
+}
+
+const char *st_variant_name(int bit) { return st::variant_name(bit); }
+
 int st_setup(const st_params *p, st_handle **out) {
     if (!p || !out) return fail(1, "null argument");
     *out = nullptr;

@@ -164,6 +164,8 @@ void launch_space_transfer(Stream st, const DevLevel &F, const DevLevel &C, int 
 void launch_reduce(Stream st, int n, const double *partial, double *out);
 int launch_norm2(Stream st, size_t n, const double *v, double *partial);
 int residual_partials(const DevLevel &L);
+unsigned long long variants(bool reset);   // bit i set: variant_name(i) has run in this process
+const char *variant_name(int bit);
 
 // setup.cpp
 TimeMats time_matrices(int q);

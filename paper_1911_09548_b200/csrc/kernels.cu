@@ -16,6 +16,7 @@
 // end value of slab k-1) and (Ct^{-1} e_0)_q = 1, checked in setup (R2).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
@@ -24,6 +25,31 @@
 #include "march.cuh"
 
 namespace st {
+
+// ------------------------------------------------------------ variant log
+// Which kernel instantiations / code paths have run in this process (st_kernel_variants): lets
+// the parity tests prove that the paths the bench takes (4 slabs per lane, several slab chunks
+// per row, multi-chunk Sigma_t carries, ...) were the ones compared with the oracle.
+static const char *const kVariantNames[] = {
+    "residual/dict", "residual/plain", "residual/plain-fold", "residual/spl1", "residual/spl2",
+    "residual/chunked", "sweep/dict", "sweep/plain", "sweep/spl1", "sweep/spl2", "sweep/spl4",
+    "sweep/chunked", "res_mass/spl1", "res_mass/spl2", "res_mass/spl4", "res_mass/chunked",
+    "gtr/fused", "gtr/chunked", "gt/two-pass", "node_scan/multichunk", "node_scan/carry-in",
+    "march/residual", "march/sweep", "restrict/space", "prolong/space", "stencil/residual",
+    "stencil/sweep", "stencil/res_mass", "coupling/prev"};
+constexpr int kNumVariants = (int)(sizeof(kVariantNames) / sizeof(kVariantNames[0]));
+static std::atomic<unsigned long long> g_variants{0};
+static inline void note(int bit) { g_variants.fetch_or(1ull << bit, std::memory_order_relaxed); }
+enum VariantBit {
+    V_RES_DICT, V_RES_PLAIN, V_RES_FOLD, V_RES_SPL1, V_RES_SPL2, V_RES_CHUNKED, V_SWEEP_DICT, V_SWEEP_PLAIN,
+    V_SWEEP_SPL1, V_SWEEP_SPL2, V_SWEEP_SPL4, V_SWEEP_CHUNKED, V_RM_SPL1, V_RM_SPL2, V_RM_SPL4, V_RM_CHUNKED,
+    V_GTR_FUSED, V_GTR_CHUNKED, V_GT_TWOPASS, V_SCAN_MULTI, V_SCAN_CARRY, V_MARCH_RES, V_MARCH_SWEEP,
+    V_RESTRICT_SPACE, V_PROLONG_SPACE, V_STENCIL_RES, V_STENCIL_SWEEP, V_STENCIL_RM, V_COUPLING_PREV
+};
+unsigned long long variants(bool reset) {
+    return reset ? g_variants.exchange(0) : g_variants.load();
+}
+const char *variant_name(int bit) { return bit >= 0 && bit < kNumVariants ? kVariantNames[bit] : nullptr; }
 
 KT make_kt(const TimeMats &tm) {
     KT k{};
@@ -1254,6 +1280,7 @@ static inline int grid(const MarchMap &mm) { return mm.n_pblocks * ((mm.S + mm.s
 int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
                     const double *prev, double *r, double *z, double omega_s, double *partial) {
     if (L.use_march && Q <= 2) {
+        note(V_MARCH_RES);
         const MarchMap mm = march_map(L, true);
         const int g = grid(mm);
         const int nt = 32 * kMarchWarps;
@@ -1274,6 +1301,11 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
     const BoxMap m = edge_map(L);
     const int g = grid(m);
     const MKELL MK{L.mk_col, L.mk_val, L.mk_width, L.mk_pk, L.mk_tab};
+    note(MK.pk && (L.M.width == 9 || L.M.width == 3) ? V_RES_DICT : V_RES_PLAIN);
+    if (!MK.pk && L.M.width == 33 && L.mk_width == 33) note(V_RES_FOLD);
+    note(m.spl == 2 ? V_RES_SPL2 : V_RES_SPL1);
+    if (m.n_chunks > 1) note(V_RES_CHUNKED);
+    if (prev) note(V_COUPLING_PREV);
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, ST_DISPATCH_W(L.M.width, L.mk_width, {
         if (partial) {
             if (r) k_residual<QQ, SP, WM_, WK_, true, false, true, true, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, x, f, prev, r, z, L.dM, L.dK, omega_s, kt, partial);
@@ -1296,6 +1328,7 @@ int residual_partials(const DevLevel &L) {
 void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, bool recon, const double *z,
                   const double *r, double *out, double omega_s, double omega) {
     if (L.use_march && Q <= 2) {
+        note(V_MARCH_SWEEP);
         const MarchMap mm = march_map(L, false);
         const int g = grid(mm), nt = 32 * kMarchWarps;
         ST_DISPATCH_Q12(Q, {
@@ -1316,6 +1349,9 @@ void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, 
     const BoxMap m = edge_map(L, dict ? 2 : plain_spl);
     const int g = grid(m);
     const MKELL MK{L.mk_col, L.mk_val, L.mk_width, dict ? L.mk_pk : nullptr, L.mk_tab};
+    note(MK.pk && (L.M.width == 9 || L.M.width == 3) ? V_SWEEP_DICT : V_SWEEP_PLAIN);
+    note(m.spl == 4 ? V_SWEEP_SPL4 : m.spl == 2 ? V_SWEEP_SPL2 : V_SWEEP_SPL1);
+    if (m.n_chunks > 1) note(V_SWEEP_CHUNKED);
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL4(m.spl, ST_DISPATCH_W(L.M.width, L.mk_width, {
         if (last && recon) k_sweep<QQ, SP, WM_, WK_, true, true, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
         else if (last) k_sweep<QQ, SP, WM_, WK_, true, false, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
@@ -1332,6 +1368,9 @@ void launch_axpy(Stream st, size_t n, double alpha, const double *z, double *x) 
 void launch_gtr(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f, const double *prev,
                 double omega_n, double *zn, double *w) {
     const BoxMap m = make_boxmap(L.S, L.sched_n, L.bptr_n, L.nbox_n, L.lpr_log2);
+    note(V_GTR_FUSED);
+    if (m.n_chunks > 1) note(V_GTR_CHUNKED);
+    if (prev) note(V_COUPLING_PREV);
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, {
         if (w) k_gtr<QQ, SP, true><<<grid(m), kBlock, 0, st>>>(m, L.GT, L.GtM, x, f, prev, L.dN, omega_n, kt, zn, w);
         else k_gtr<QQ, SP, false><<<grid(m), kBlock, 0, st>>>(m, L.GT, L.GtM, x, f, prev, L.dN, omega_n, kt, zn, w);
@@ -1343,6 +1382,9 @@ void launch_res_mass(Stream st, const DevLevel &L, const KT &kt, int Q, const do
     // 4 slabs per lane: measured 68 vs 75 ms per 5 c4 V-cycles at 2 (env ST_RESMASS_SPL)
     static const int spl = std::getenv("ST_RESMASS_SPL") ? std::atoi(std::getenv("ST_RESMASS_SPL")) : 4;
     const BoxMap m = edge_map(L, spl);
+    note(m.spl == 4 ? V_RM_SPL4 : m.spl == 2 ? V_RM_SPL2 : V_RM_SPL1);
+    if (m.n_chunks > 1) note(V_RM_CHUNKED);
+    if (prev) note(V_COUPLING_PREV);
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL4(m.spl, {
         if (L.M.width == 9) k_res_mass<QQ, SP, 9><<<grid(m), kBlock, 0, st>>>(m, L.M, x, f, prev, u, kt);
         else if (L.M.width == 3) k_res_mass<QQ, SP, 3><<<grid(m), kBlock, 0, st>>>(m, L.M, x, f, prev, u, kt);
@@ -1352,6 +1394,7 @@ void launch_res_mass(Stream st, const DevLevel &L, const KT &kt, int Q, const do
 
 void launch_gt(Stream st, const DevLevel &L, int Q, const double *u, double omega_n, double *zn, double *w) {
     const BoxMap m = make_boxmap(L.S, L.sched_n, L.bptr_n, L.nbox_n, L.lpr_log2);
+    note(V_GT_TWOPASS);
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, {
         if (w) k_gt<QQ, SP, true><<<grid(m), kBlock, 0, st>>>(m, L.GT, u, L.dN, omega_n, zn, w);
         else k_gt<QQ, SP, false><<<grid(m), kBlock, 0, st>>>(m, L.GT, u, L.dN, omega_n, zn, w);
@@ -1368,6 +1411,8 @@ void launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mod
                       const double *w, double omega_n, const double *carry, double *y, double *tot) {
     const int g = nblocks((long long)L.n_nodes * 32);
     const int spl = L.S % 2 == 0 ? 2 : 1;
+    if (L.S > 32 * spl) note(V_SCAN_MULTI);
+    if (carry) note(V_SCAN_CARRY);
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(spl, {
         if (mode == 0) k_node_scan<QQ, SP, 0><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
         else if (mode == 1) k_node_scan<QQ, SP, 1><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
@@ -1392,6 +1437,7 @@ void launch_end_values(Stream st, int rows, int Q, int S, const double *x, doubl
 
 void launch_restrict(Stream st, const DevLevel &F, const DevLevel &C, int Q, const double *r, double *fc) {
     const Map m = make_map(C.n_edges, C.S, false);
+    if (F.space_coarsened) note(V_RESTRICT_SPACE);
     ST_DISPATCH_Q(Q, {
         if (F.space_coarsened) k_restrict<QQ, true><<<grid(m), kBlock, 0, st>>>(m, F.Rg, r, F.Pt, fc);
         else k_restrict<QQ, false><<<grid(m), kBlock, 0, st>>>(m, F.Rg, r, F.Pt, fc);
@@ -1400,6 +1446,7 @@ void launch_restrict(Stream st, const DevLevel &F, const DevLevel &C, int Q, con
 
 void launch_prolong(Stream st, const DevLevel &F, int Q, const double *xc, double *x) {
     const Map m = make_map(F.n_edges, F.S / 2, false);
+    if (F.space_coarsened) note(V_PROLONG_SPACE);
     ST_DISPATCH_Q(Q, {
         if (F.space_coarsened) k_prolong<QQ, true><<<grid(m), kBlock, 0, st>>>(m, F.Pg, xc, F.Pt, x);
         else k_prolong<QQ, false><<<grid(m), kBlock, 0, st>>>(m, F.Pg, xc, F.Pt, x);

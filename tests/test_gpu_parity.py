@@ -14,6 +14,11 @@ RTOL = 1e-10
 # error of about (nnz per row) * eps * ||f|| ~ 1e-14 ||f|| (tolerance derivation), so
 # two correct implementations agree to RTOL relative OR to that rounding floor, whichever is larger.
 ATOL_FLOOR = 1e-14
+# Tolerance multiplier on the oracle's one-ulp sensitivity ("noise"): measured against an
+# extended-precision evaluation, the fp64 oracle's true error is 0.7-1.2x its noise on every recipe
+# (tests/test_oracle_precision.py, R12), so two correct fp64 implementations differ by at
+# most ~2.4x noise; 10x leaves margin (round 1 used an unexplained 50x for the histories).
+NOISE_MULT = 10.0
 
 
 @pytest.fixture(scope="module")
@@ -77,13 +82,13 @@ def test_solve_parity(torch_cuda, name, maxit):
     x = torch.zeros_like(f)
     it, h = s.solve(x, f, tol=1e-8, maxit=maxit)
     assert it == len(hist) - 1
-    tol = np.maximum(np.maximum(RTOL * np.array(hist), ATOL_FLOOR), 50 * noise)
+    tol = np.maximum(np.maximum(RTOL * np.array(hist), ATOL_FLOOR), NOISE_MULT * noise)
     diff = np.abs(np.array(h) - np.array(hist))
     print(name, "max diff/tol", float(np.max(diff / tol)), "max rel diff", float(np.max(diff / np.array(hist))))
     assert np.all(diff <= tol), (diff, tol)
     Xg = workloads.to_oracle(x.cpu().numpy())
     xnoise = np.linalg.norm(Xn - X)
-    assert np.linalg.norm(Xg - X) <= max(1e-9 * np.linalg.norm(X), 20 * xnoise)
+    assert np.linalg.norm(Xg - X) <= max(1e-9 * np.linalg.norm(X), NOISE_MULT * xnoise)
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c5"])
@@ -106,7 +111,7 @@ def test_vcycle_parity_random_start(torch_cuda, name, q):
     Xg = workloads.to_oracle(x.cpu().numpy())
     err = np.linalg.norm(Xg - X1)
     print(name, q, "err", err / np.linalg.norm(X1), "noise", noise / np.linalg.norm(X1))
-    assert err <= max(1e-12 * np.linalg.norm(X1), 20 * noise)
+    assert err <= max(1e-12 * np.linalg.norm(X1), NOISE_MULT * noise)
 
 
 @pytest.mark.parametrize("name", ["c1", "c4", "c3"])
@@ -135,7 +140,7 @@ def test_march_matches_ell_and_oracle(torch_cuda, name, q):
         Xg = workloads.to_oracle(x.cpu().numpy())
         err = np.linalg.norm(Xg - X1)
         print(name, q, "path", path, "err", err / np.linalg.norm(X1), "noise", noise / np.linalg.norm(X1))
-        assert err <= max(1e-12 * np.linalg.norm(X1), 20 * noise)
+        assert err <= max(1e-12 * np.linalg.norm(X1), NOISE_MULT * noise)
     R = F - st_oracle.apply_L(H.levels[0], X0)
     for Rg in outs:
         np.testing.assert_allclose(Rg, R, rtol=0, atol=1e-12 * np.abs(R).max())
@@ -157,7 +162,7 @@ def test_vcycle_parity_smoother_variants(torch_cuda, spec, nu_s, nu_n):
     Xg = workloads.to_oracle(x.cpu().numpy())
     err = np.linalg.norm(Xg - X1)
     print(spec, nu_s, nu_n, "err", err / np.linalg.norm(X1), "noise", noise / np.linalg.norm(X1))
-    assert err <= max(1e-12 * np.linalg.norm(X1), 20 * noise)
+    assert err <= max(1e-12 * np.linalg.norm(X1), NOISE_MULT * noise)
 
 
 @pytest.mark.parametrize("name", ["c1", "c3", "c5"])
