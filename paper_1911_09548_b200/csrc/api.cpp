@@ -14,6 +14,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -62,9 +63,12 @@ struct st_handle {
     int64_t n_dofs = 0;
     // CUDA-graph replay of the single-process V-cycle (st_set_graphs)
     bool use_graphs = false;
-    bool gtr_two_pass = true;
+    int nodal_res = 0;          // env ST_NODAL_RES: 0 G^T (f - L x) literally (default), 1 two-pass
+                                // with G^T K = 0 (u = f - Ct M x), 2 fused node-row G^T M (K G = 0)
     bool mk_dict = true;        // env ST_MK_DICT=0: never use the dictionary ELL
-    std::vector<int> tab_slots;   // env ST_GTR_TWO_PASS=0: always the fused node-row G^T M kernel
+    bool stencil = true;        // env ST_STENCIL=0: never use the structured stencil march
+    std::vector<std::unique_ptr<st::StencilTab>> st_tabs;
+    std::vector<int> tab_slots;   // constant-bank dictionary slots this handle holds
     cudaStream_t cap_stream = nullptr;
     struct Graph { const double *x, *f; cudaGraphExec_t exec; int64_t launches; };
     std::vector<Graph> graphs;
@@ -96,19 +100,19 @@ struct st_handle {
     void run(const char *fam, double bytes, int count, F &&launch) {
         if (debug_sync) {
             launch();
-            launches += count;
+            launches += count + st::take_extra_launches();
             cudaError_t e = cudaStreamSynchronize(stream);
             if (e == cudaSuccess) e = cudaGetLastError();
             if (e != cudaSuccess) throw CudaError(std::string("kernel ") + fam + ": " + cudaGetErrorString(e));
             return;
         }
-        if (!prof) { launch(); launches += count; return; }
+        if (!prof) { launch(); launches += count + st::take_extra_launches(); return; }
         Rec r{fam_id(fam), bytes, ev(), ev()};
         ck(cudaEventRecord(r.a, stream), "event record");
         launch();
         ck(cudaEventRecord(r.b, stream), "event record");
         recs.push_back(r);
-        launches += count;
+        launches += count + st::take_extra_launches();
     }
 
     template <class T>
@@ -300,7 +304,17 @@ void correct_A_local(st_handle *h, DevLevel &L, double *x, const double *f, cons
     auto s = (st::Stream)h->stream;
     const int Q = h->Q;
     const double ev = evec(L, Q), nv = nvec(L, Q), kb = ell_bytes(L.Kn) + 8.0 * L.n_nodes;
-    if (h->gtr_two_pass && L.M.width <= 12) {
+    if (h->nodal_res == 0) {
+        // Eq. (5) as written: r = f - L x with the full operator, then w = G^T r
+        // on node rows (6 gathers).  The K G = 0 shortcuts below are the same map in exact
+        // arithmetic but drop G^T K x, which in fp64 is rounding of size eps |tau K x|: measured
+        // against an extended-precision V-cycle they are 7-13x less accurate than this form on the
+        // c5 / c3 recipes (R12, tests/test_gpu_bench_paths.py)
+        h->run("residual", 3 * ev + op_bytes(L), 1,
+               [&] { st::launch_residual(s, L, h->kt, Q, x, f, prev, L.r, nullptr, o.omega_s, nullptr); });
+        h->run("gt", ev + (o.nu_n > 2 ? 2 : 1) * nv + 8.0 * L.n_nodes, 1,
+               [&] { st::launch_gt(s, L, Q, L.r, o.omega_n, L.zn, o.nu_n > 2 ? L.wn : nullptr); });
+    } else if (h->nodal_res == 1 && L.M.width <= 12) {
         // narrow M (uniform meshes): u = f - (Ct (x) M) x + coupling on edge rows, then w = G^T u
         // on node rows (6 gathers) -- one more vector pass, far fewer L1 gathers than G^T M
         h->run("gtr_mass", 3 * ev + ell_bytes(L.M), 1, [&] { st::launch_res_mass(s, L, h->kt, Q, x, f, prev, L.r); });
@@ -547,8 +561,9 @@ int st_setup(const st_params *p, st_handle **out) {
         ck(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
         h->own_stream = true;
         if (const char *dbg = std::getenv("ST_DEBUG_SYNC")) h->debug_sync = dbg[0] == '1';
-        if (const char *tp = std::getenv("ST_GTR_TWO_PASS")) h->gtr_two_pass = tp[0] != '0';
+        if (const char *nr = std::getenv("ST_NODAL_RES")) h->nodal_res = std::atoi(nr);
         if (const char *md = std::getenv("ST_MK_DICT")) h->mk_dict = md[0] != '0';
+        if (const char *sv = std::getenv("ST_STENCIL")) h->stencil = sv[0] != '0';
         size_t max_partial = 1;
         auto build = [&](int l, int b, int cnt, bool coarsest, bool alloc_x) {
             st::HostLevel &H = h->hl[l];
@@ -565,6 +580,19 @@ int st_setup(const st_params *p, st_handle **out) {
             D.sched_n = h->upload(H.sched_n); D.bptr_n = h->upload(H.bptr_n);
             D.nbox_e = (int)H.bptr_e.size() - 1; D.nbox_n = (int)H.bptr_n.size() - 1;
             D.tau = h->upload(std::vector<double>(H.tau.begin() + b, H.tau.begin() + b + cnt));
+            // structured stencil march (stencil.cuh) on class-uniform hex levels whose slab count
+            // fills whole warps; env ST_STENCIL=0 keeps the ELL kernels (measurements)
+            if (h->stencil && o.kernel_path == 0 && (Q == 1 || Q == 2) && cnt % (32 / Q) == 0 && H.uniform &&
+                H.mesh.dim == 3) {
+                auto tab = std::make_unique<st::StencilTab>();
+                if (st::build_stencil_tab(H, *tab)) {
+                    D.use_stencil = true;
+                    D.st_tab = tab.get();
+                    h->st_tabs.push_back(std::move(tab));
+                    D.grid.nx = H.mesh.n[0]; D.grid.ny = H.mesh.n[1]; D.grid.nz = H.mesh.n[2];
+                    D.grid.Ex = H.mesh.Ex; D.grid.Ey = H.mesh.Ey;
+                }
+            }
             D.space_coarsened = H.space_coarsened;
             if (const char *e = std::getenv("ST_EDGE_LPR")) D.lpr_log2 = std::max(0, std::min(5, std::atoi(e)));
             // the march uses 32-bit element offsets

@@ -73,6 +73,32 @@ struct HostLevel {
     double hbox[3] = {0, 0, 0};
 };
 
+// Structured stencil table (stencil.cuh): (M, K) coefficients per edge direction T, boundary class
+// (3 x 3: the two transverse coordinates at 0 / inside / at n) and structural slot (33).  Passed to
+// the kernels by value (kernel parameter space, 14256 bytes).
+constexpr int kStClasses = 9, kStSlots = 33;
+struct StencilTab {
+    double2 c[3][kStClasses][kStSlots];
+};
+bool build_stencil_tab(const HostLevel &L, StencilTab &tab);   // false: the level is not class-uniform
+
+// Slot numbering of the stencil table: for a row of direction T at node p, neighbour edge of
+// direction T2 at node p + (o0, o1, o2); block of T2 == T: o_T = 0, the other two offsets in
+// {-1,0,1} (9 slots); T2 != T: o_T in {0,1}, o_T2 in {-1,0}, the third in {-1,0,1} (12 slots);
+// blocks ordered T2 = 0, 1, 2.
+__host__ __device__ constexpr int st_slot(int T, int T2, int o0, int o1, int o2) {
+    // block start (blocks of the directions before T2), then the position inside the block
+    return ((T2 > 0 ? (T == 0 ? 9 : 12) : 0) + (T2 > 1 ? (T == 1 ? 9 : 12) : 0)) +
+           (T2 == T
+                ? (T == 0 ? (o1 + 1) * 3 + (o2 + 1) : T == 1 ? (o0 + 1) * 3 + (o2 + 1) : (o0 + 1) * 3 + (o1 + 1))
+                : ((T == 0 ? o0 : T == 1 ? o1 : o2) * 6 + ((T2 == 0 ? o0 : T2 == 1 ? o1 : o2) + 1) * 3 +
+                   ((3 - T - T2 == 0 ? o0 : 3 - T - T2 == 1 ? o1 : o2) + 1)));
+}
+
+// boundary class of a coordinate v in [0, n]: 0 at 0, 2 at n, 1 inside
+__host__ __device__ __forceinline__ int st_cls(int v, int n) { return v <= 0 ? 0 : (v >= n ? 2 : 1); }
+
+
 // uniform axis-aligned hex level for the matrix-free pencil march (march.cuh)
 struct Grid3 {
     int nx, ny, nz, Ex, Ey;
@@ -94,6 +120,8 @@ struct DevLevel {
     int *sched_e = nullptr, *bptr_e = nullptr, *sched_n = nullptr, *bptr_n = nullptr;
     int nbox_e = 0, nbox_n = 0;
     bool use_march = false;
+    bool use_stencil = false;       // structured stencil march (stencil.cuh) for residual and sweep
+    StencilTab *st_tab = nullptr;   // host copy of the level's stencil table (owned by the handle)
     int lpr_log2 = 5;       // edge kernels: log2(lanes per row); slab chunk = 2 << lpr_log2 (32: measured best)
     Grid3 grid{};
     double *tau = nullptr;
@@ -164,6 +192,8 @@ void launch_space_transfer(Stream st, const DevLevel &F, const DevLevel &C, int 
 void launch_reduce(Stream st, int n, const double *partial, double *out);
 int launch_norm2(Stream st, size_t n, const double *v, double *partial);
 int residual_partials(const DevLevel &L);
+bool stencil_applies(const DevLevel &L, int Q);
+int take_extra_launches();   // launches issued beyond the count the caller passes to run()
 unsigned long long variants(bool reset);   // bit i set: variant_name(i) has run in this process
 const char *variant_name(int bit);
 

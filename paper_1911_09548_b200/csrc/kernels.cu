@@ -1187,8 +1187,31 @@ __global__ void __launch_bounds__(1024) k_reduce(int n, const double *__restrict
     if (threadIdx.x == 0) *out = v;
 }
 
+#include "stencil.cuh"
+
 // --------------------------------------------------------------- launchers
 static inline int nblocks(long long work) { return (int)((work + kBlock - 1) / kBlock); }
+
+// launches issued by a launcher beyond the one its caller counts (the stencil coupling pre-pass)
+static thread_local int g_extra_launches = 0;
+int take_extra_launches() { const int n = g_extra_launches; g_extra_launches = 0; return n; }
+
+static StGeo stencil_geo(const DevLevel &L, int Q) {
+    StGeo g{};
+    g.nx = L.grid.nx; g.ny = L.grid.ny; g.nz = L.grid.nz; g.Ex = L.grid.Ex; g.Ey = L.grid.Ey;
+    g.S = L.S;
+    g.tiles_i = (g.nx + 1 + kStTI - 1) / kStTI;
+    const int tiles_j = (g.ny + 1 + kStTJ - 1) / kStTJ;
+    g.n_tiles = g.tiles_i * tiles_j;
+    g.n_chunks = L.S / (32 / Q);
+    return g;
+}
+static inline int grid(const StGeo &g) { return g.n_tiles * g.n_chunks; }
+
+bool stencil_applies(const DevLevel &L, int Q) {
+    return L.use_stencil && L.st_tab && (Q == 1 || Q == 2) && L.S % (32 / Q) == 0;
+}
+
 
 static Map make_map(int rows, int S, bool allow_pairs = true) {
     Map m{};
@@ -1279,6 +1302,25 @@ static inline int grid(const MarchMap &mm) { return mm.n_pblocks * ((mm.S + mm.s
 
 int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
                     const double *prev, double *r, double *z, double omega_s, double *partial) {
+    if (stencil_applies(L, Q)) {
+        note(V_STENCIL_RES);
+        if (prev) note(V_COUPLING_PREV);
+        const StGeo g = stencil_geo(L, Q);
+        const int nb = grid(g), nt = 32 * kStWarps;
+        ST_DISPATCH_Q12(Q, {
+            if (partial) {
+                if (r) k_st_residual<QQ, true, false, true><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, x, f, prev, r, z, omega_s, kt, partial);
+                else k_st_residual<QQ, false, false, true><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, x, f, prev, r, z, omega_s, kt, partial);
+            } else if (r && z) {
+                k_st_residual<QQ, true, true, false><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, x, f, prev, r, z, omega_s, kt, partial);
+            } else if (z) {
+                k_st_residual<QQ, false, true, false><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, x, f, prev, r, z, omega_s, kt, partial);
+            } else {
+                k_st_residual<QQ, true, false, false><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, x, f, prev, r, z, omega_s, kt, partial);
+            }
+        });
+        return nb;
+    }
     if (L.use_march && Q <= 2) {
         note(V_MARCH_RES);
         const MarchMap mm = march_map(L, true);
@@ -1322,11 +1364,24 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
 }
 
 int residual_partials(const DevLevel &L) {
+    if (stencil_applies(L, L.Q)) return grid(stencil_geo(L, L.Q));
     return (L.use_march && L.Q <= 2) ? grid(march_map(L, true)) : grid(edge_map(L));
 }
 
 void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, bool recon, const double *z,
                   const double *r, double *out, double omega_s, double omega) {
+    if (stencil_applies(L, Q)) {
+        note(V_STENCIL_SWEEP);
+        const StGeo g = stencil_geo(L, Q);
+        const int nb = grid(g), nt = 32 * kStWarps;
+        ST_DISPATCH_Q12(Q, {
+            if (last && recon) k_st_sweep<QQ, true, true><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, z, r, out, omega_s, omega, kt);
+            else if (last) k_st_sweep<QQ, true, false><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, z, r, out, omega_s, omega, kt);
+            else if (recon) k_st_sweep<QQ, false, true><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, z, r, out, omega_s, omega, kt);
+            else k_st_sweep<QQ, false, false><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, z, r, out, omega_s, omega, kt);
+        });
+        return;
+    }
     if (L.use_march && Q <= 2) {
         note(V_MARCH_SWEEP);
         const MarchMap mm = march_map(L, false);

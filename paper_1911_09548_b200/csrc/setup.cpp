@@ -630,6 +630,88 @@ static void detect_uniform(HostLevel &L) {
     for (int a = 0; a < 3; ++a) L.hbox[a] = h[a];
 }
 
+// Structured stencil table (stencil.cuh): on a uniform hex level, every edge row's merged (M, K)
+// entries are mapped to structural slots; rows of one (direction, boundary class) must carry
+// bitwise identical coefficients, M must vanish off the parallel block (axis-aligned cells), and a
+// slot whose neighbour does not exist must be zero for the whole class.  Returns false (the level
+// keeps the ELL kernels) when any of this fails, e.g. for per-cell varying coefficients.
+bool build_stencil_tab(const HostLevel &L, StencilTab &tab) {
+    const HostMesh &m = L.mesh;
+    if (m.dim != 3 || !L.uniform || L.MK.rows != m.n_edges) return false;
+    const int nx = m.n[0], ny = m.n[1], nz = m.n[2];
+    const int W = L.MK.width;
+    std::memset(&tab, 0, sizeof(tab));
+    bool seen[3][kStClasses] = {};
+    auto decode = [&](int e, int &T, int &i, int &j, int &l) {
+        if (e < m.Ex) { T = 0; i = e % nx; j = (e / nx) % (ny + 1); l = e / (nx * (ny + 1)); }
+        else if (e < m.Ex + m.Ey) { const int f = e - m.Ex; T = 1; i = f % (nx + 1); j = (f / (nx + 1)) % ny; l = f / ((nx + 1) * ny); }
+        else { const int f = e - m.Ex - m.Ey; T = 2; i = f % (nx + 1); j = (f / (nx + 1)) % (ny + 1); l = f / ((nx + 1) * (ny + 1)); }
+    };
+    auto exists = [&](int T, int i, int j, int l) {
+        if (i < 0 || j < 0 || l < 0 || i > nx || j > ny || l > nz) return false;
+        return T == 0 ? i < nx : (T == 1 ? j < ny : l < nz);
+    };
+    double2 row[kStSlots];
+    bool has[kStSlots];
+    for (int r = 0; r < m.n_edges; ++r) {
+        int T, i, j, l;
+        decode(r, T, i, j, l);
+        const int cls = T == 0 ? 3 * st_cls(j, ny) + st_cls(l, nz)
+                               : (T == 1 ? 3 * st_cls(i, nx) + st_cls(l, nz) : 3 * st_cls(i, nx) + st_cls(j, ny));
+        for (int s2 = 0; s2 < kStSlots; ++s2) { row[s2] = make_double2(0.0, 0.0); has[s2] = false; }
+        for (int s = 0; s < W; ++s) {
+            const size_t o = (size_t)r * W + s;
+            const double mv = L.MK.val[o], kv = L.MKk[o];
+            if (mv == 0.0 && kv == 0.0) continue;        // padding (col = row, value 0)
+            int T2, i2, j2, l2;
+            decode(L.MK.col[o], T2, i2, j2, l2);
+            const int o0 = i2 - i, o1 = j2 - j, o2 = l2 - l;
+            const int oT = T == 0 ? o0 : (T == 1 ? o1 : o2);
+            const int oT2 = T2 == 0 ? o0 : (T2 == 1 ? o1 : o2);
+            const int t3 = 3 - T - T2;
+            const int o3 = t3 == 0 ? o0 : (t3 == 1 ? o1 : o2);
+            if (T2 == T) {
+                if (oT != 0) return false;
+                for (int a = 0; a < 3; ++a)
+                    if (a != T && std::abs(a == 0 ? o0 : (a == 1 ? o1 : o2)) > 1) return false;
+            } else {
+                if (oT < 0 || oT > 1 || oT2 < -1 || oT2 > 0 || o3 < -1 || o3 > 1) return false;
+                if (mv != 0.0) return false;                 // M couples parallel edges only here
+            }
+            const int sl = st_slot(T, T2, o0, o1, o2);
+            if (has[sl]) return false;
+            has[sl] = true;
+            row[sl] = make_double2(mv, kv);
+        }
+        double2 *t = tab.c[T][cls];
+        if (!seen[T][cls]) {
+            seen[T][cls] = true;
+            for (int s2 = 0; s2 < kStSlots; ++s2) t[s2] = row[s2];
+        } else {
+            for (int s2 = 0; s2 < kStSlots; ++s2)
+                if (std::memcmp(&t[s2], &row[s2], sizeof(double2)) != 0) return false;
+        }
+    }
+    // every nonzero slot of a class must point at an existing edge for every row of the class
+    for (int r = 0; r < m.n_edges; ++r) {
+        int T, i, j, l;
+        decode(r, T, i, j, l);
+        const int cls = T == 0 ? 3 * st_cls(j, ny) + st_cls(l, nz)
+                               : (T == 1 ? 3 * st_cls(i, nx) + st_cls(l, nz) : 3 * st_cls(i, nx) + st_cls(j, ny));
+        for (int T2 = 0; T2 < 3; ++T2)
+            for (int o0 = -1; o0 <= 1; ++o0)
+                for (int o1 = -1; o1 <= 1; ++o1)
+                    for (int o2 = -1; o2 <= 1; ++o2) {
+                        const int oT = T == 0 ? o0 : (T == 1 ? o1 : o2);
+                        const int oT2 = T2 == 0 ? o0 : (T2 == 1 ? o1 : o2);
+                        if (T2 == T ? oT != 0 : (oT < 0 || oT2 > 0)) continue;
+                        const double2 c = tab.c[T][cls][st_slot(T, T2, o0, o1, o2)];
+                        if ((c.x != 0.0 || c.y != 0.0) && !exists(T2, i + o0, j + o1, l + o2)) return false;
+                    }
+    }
+    return true;
+}
+
 // Spatial coarsening chain of the finest mesh for the inner V-cycle (R13): chain[i] is the
 // mesh coarsened i times (coefficients averaged as for the outer hierarchy, R6), with the
 // transfers chain[i] -> chain[i+1] in chain[i].Pg / Rg.  Every outer level's mesh is one of

@@ -78,7 +78,10 @@ def _worker(rank, P, port, name, out, opts=None):
 
 
 @pytest.mark.parametrize("name,P,opts", [("c1", 2, {}), ("c4", 2, {}), ("c5", 2, {}), ("c1", 4, {}),
-                                         ("c4", 2, {"inner": "mg"})])
+                                         ("c4", 2, {"inner": "mg"}),
+                                         # 16 slabs per rank: the stencil march with the previous
+                                         # rank's end values as the upwind coupling of slab 0
+                                         ("c4_s32", 2, {})])
 def test_two_ranks_one_gpu(name, P, opts):
     import torch.multiprocessing as mp
     import paper_1911_09548_b200 as p
@@ -101,7 +104,7 @@ def test_two_ranks_one_gpu(name, P, opts):
     f = torch.from_numpy(F).cuda()
     s.vcycle(x, f)
     Xs = x.cpu().numpy()
-    tol = 1e-11 if name == "c5" else 1e-12
+    tol = 1e-11 if name == "c5" else 1e-12          # same kernels, the halo only moves a trace
     assert np.linalg.norm(Xd - Xs) <= tol * np.linalg.norm(Xs)
     x.zero_()
     it, h1 = s.solve(x, f, tol=1e-10, maxit=5)

@@ -60,8 +60,11 @@ def _to_csr(rows, width, col, val, ncols):
     return sp.csr_matrix((val.ravel(), (r, col.ravel())), shape=(rows, ncols))
 
 
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c5"])
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
 def test_host_operators_match_oracle(stlib, name):
+    # The C++ setup and the oracle assemble M, K, K_n independently (different quadrature loops and
+    # summation orders): every entry agrees to <= 32 ulps of its row's largest entry (measured <= 16).
+    # This is the operator-rounding model behind the parity envelope (tests/parity_util.py).
     w = workloads.small(name)
     a, kw = _args(w)
     H = mg.Hierarchy(mesh.Mesh(w.n, w.node_coords()), w.sigma, w.nu, w.tau, w.q, mg.Options(omega_s=w.omega_s))
@@ -69,7 +72,10 @@ def test_host_operators_match_oracle(stlib, name):
         lv = H.levels[lvl]
         for which, ref, ncols in ((0, lv.M, lv.n), (1, lv.K, lv.n), (2, lv.Kn, lv.nn)):
             A = _to_csr(*stlib.host_matrix(lvl, which, *a, **kw), ncols)
-            assert abs(A - ref).max() <= 1e-13 * abs(ref).max(), (name, lvl, which)
+            D = (A - ref).tocoo()
+            rowmax = np.asarray(abs(ref).max(axis=1).todense()).ravel()
+            ulps = np.abs(D.data) / np.spacing(rowmax[D.row]) if D.nnz else np.zeros(1)
+            assert ulps.max() <= 32, (name, lvl, which, ulps.max())
         if lvl < len(H.levels) - 1 and H.P_edge[lvl] is not None:
             P = _to_csr(*stlib.host_matrix(lvl, 3, *a, **kw), H.levels[lvl + 1].n)
             assert abs(P - H.P_edge[lvl]).max() == 0.0
