@@ -109,21 +109,45 @@ def measured_peak():
 
 
 def ncu_traffic(family):
-    """dram__bytes_read.sum + dram__bytes_write.sum of the finest-level launch of `family` from the
-    committed ncu --set full capture of the current kernels (profiles/r01_ncu_v6_kernels.json), or None."""
-    p = os.path.join(ROOT, "profiles", "r01_ncu_v6_kernels.json")
+    """(dram__bytes_read.sum + dram__bytes_write.sum, source) of the finest-level launch of the
+    family's kernel in the committed `ncu --set full` capture of the bench command
+    (profiles/r02_ncu_kernels.json, scripts/ncu_summary.py), or (None, why) when the capture was
+    taken from other kernel sources than the ones built now (its source hash differs)."""
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    from srchash import srchash
+    p = os.path.join(ROOT, "profiles", "r02_ncu_kernels.json")
     if not os.path.exists(p):
-        return None
-    tag = {"residual": "k_residual", "sweep_update": "k_sweep", "gtr": "k_gtr", "gtr_mass": "k_res_mass",
-           "gt": "k_gt", "node_scan": "k_node_scan"}.get(family)
-    with open(p) as fh:
-        for k in json.load(fh):
-            if tag and tag + "<" in k["Kernel Name"]:
-                def gb(s):
-                    v, u = s.split()[:2]
-                    return float(v) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(u, 1.0)
-                return gb(k["dram__bytes_read.sum"]) + gb(k["dram__bytes_write.sum"])
-    return None
+        return None, "no capture"
+    cap = json.load(open(p))
+    if cap.get("source_hash") != srchash():
+        return None, f"capture {os.path.basename(p)} is of other kernel sources ({cap.get('source_hash')} vs {srchash()})"
+    tags = {"residual": ("k_st_residual<", "k_residual<"), "sweep_update": ("k_st_sweep<", "k_sweep<"),
+            "node_scan": ("k_node_scan<",), "gt": ("k_gt<",)}.get(family, ())
+
+    def gb(v):
+        val, unit = v.split()[:2]
+        return float(val) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}.get(unit, 1.0)
+    for d in cap["launches"]:
+        if any(t in d["kernel"] for t in tags):
+            return (gb(d["dram__bytes_read.sum"]) + gb(d["dram__bytes_write.sum"]),
+                    f"{os.path.basename(p)} (source hash {cap['source_hash']}): {d['kernel'][:60]}, finest level")
+    return None, "family not in the capture"
+
+
+def link_bandwidth(torch, host, dev, stream):
+    """Pinned host <-> device copy bandwidth of this box per direction (GB/s), the bound of the
+    e2e number: one full-vector copy each way, CUDA events."""
+    out = {}
+    with torch.cuda.stream(stream):
+        for name, dst, src in (("h2d", dev, host), ("d2h", host, dev)):
+            dst.copy_(src, non_blocking=True)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dst.copy_(src, non_blocking=True)
+            e1.record(stream)
+            stream.synchronize()
+            out[name] = host.numel() * 8 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    return out
 
 
 # ------------------------------------------------------------- CPU oracle
@@ -240,14 +264,14 @@ def run_ours(args, rank, world, local_rank):
                 # st_solve_many_host: per step (= problem) H2D f from pinned memory, x = 0, ||f||,
                 # ||r||, one V-cycle, ||r||, D2H x; the copies of neighbouring steps overlap the solve
                 xh2 = torch.zeros(fh.shape, dtype=torch.float64).pin_memory()
-                s.solve_many_host([xh.numpy()], [fh.numpy()], tol=0.0, maxit=1)      # warm-up
+                s.solve_many_host([xh.numpy()], [fh.numpy()], tol=0.0, maxit=1, history=False)   # warm-up
                 ke = max(2, min(args.steps, 5))
                 outs = [(xh if i % 2 == 0 else xh2).numpy() for i in range(ke)]
                 t0 = time.perf_counter()
-                s.solve_many_host(outs, [fh.numpy()] * ke, tol=0.0, maxit=1)
+                s.solve_many_host(outs, [fh.numpy()] * ke, tol=0.0, maxit=1, history=False)
                 te = (time.perf_counter() - t0) / ke
                 note = (f"st_solve_many_host, {ke} steps in one call: per step H2D f from pinned memory, x = 0, "
-                        "||f||, ||r||, one V-cycle, ||r||, D2H x; copies of neighbouring steps overlap the V-cycles "
+                        "one V-cycle (tol = 0: no norms), D2H x; copies of neighbouring steps overlap the V-cycles "
                         "(the first H2D and the last D2H are not hidden and are included)")
             else:
                 def e2e_step():
@@ -269,7 +293,8 @@ def run_ours(args, rank, world, local_rank):
                 te = float(t.item())
             e2e = {"value": n_dofs * world / te, "unit": UNIT,
                    "h2d_bytes_per_step": (1 if world == 1 else 2) * f.numel() * 8 * world,
-                   "d2h_bytes_per_step": f.numel() * 8 * world, "note": note}
+                   "d2h_bytes_per_step": f.numel() * 8 * world, "note": note,
+                   "link_GBps": link_bandwidth(torch, fh, f, stream)}
     info = s.info()
     s.close()
     torch.cuda.synchronize()
@@ -277,6 +302,8 @@ def run_ours(args, rank, world, local_rank):
         return
     peak, peak_src = measured_peak()
     fam, (nl, kms, kbytes) = max(kstats.items(), key=lambda kv: kv[1][1])
+    traffic, traffic_src = ncu_traffic(fam) if (args.cells, args.slabs, world) == (64, 512, 1) else \
+        (None, "capture is of the default 64^3 x 512-slab configuration")
     dur = kms / nl
     achieved = kbytes / nl / (dur * 1e-3) / 1e9
     total_bytes = sum(v[2] for v in kstats.values())
@@ -292,7 +319,7 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"time-slab blocks over {world} GPU(s) (NCCL halo/carry/norm collectives)"
                    if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(fam), "kernel": fam, "peak_source": peak_src,
+                     "traffic": traffic, "traffic_source": traffic_src, "kernel": fam, "peak_source": peak_src,
                      "kernel_share_of_step": kms / t_max,
                      "vcycle_algorithmic_GBps": total_bytes / (t_max * 1e-3) / 1e9},
         "gpu_launches": int(launches),
@@ -309,9 +336,26 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(out), flush=True)
 
 
+def spawn(args):
+    """`--gpus N` outside torchrun: launch N ranks of this script with torch.distributed.run (one
+    process per GPU, rendezvous on 127.0.0.1) and return their exit code."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":

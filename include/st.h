@@ -126,7 +126,8 @@ int st_set_graphs(st_handle *h, int enable);
 
 /* V-cycles from the given x until ||f - L x|| <= tol ||f|| or maxit cycles.
  * Device pointers.  *iters (host) = cycles run; hist (host, maxit+1 doubles,
- * may be NULL) = relative residual before each cycle and after the last. */
+ * may be NULL) = relative residual before each cycle and after the last.
+ * tol <= 0 with hist == NULL runs exactly maxit cycles and computes no norm. */
 int st_solve(st_handle *h, double *x, const double *f, double tol, int maxit,
              int *iters, double *hist);
 
@@ -195,6 +196,12 @@ int st_lv_end_values(st_handle *h, int set, int level, const double *x, double *
 int st_copy_slabs(st_handle *h, int rows, int q, int ns, double *dst, int dS, int dk0, const double *src, int sS,
                   int sk0, int add);
 int st_zero(st_handle *h, double *ptr, int64_t n);
+/* Vector operations of the multi-GPU driver (device pointers, n elements, on the handle's stream):
+ * y += alpha x; out = sum over b < nb of the blocks in[b*n .. (b+1)*n) (the Sigma_t carry of the
+ * ranks before this one, R2; nb = 0 gives zeros); *out (host) = ||v||_2^2 (synchronises). */
+int st_vec_axpy(st_handle *h, int64_t n, double alpha, const double *x, double *y);
+int st_vec_sum_blocks(st_handle *h, int64_t n, int nb, const double *in, double *out);
+int st_vec_norm2(st_handle *h, int64_t n, const double *v, double *out);
 int st_sync(st_handle *h);
 
 /* Host-only (no CUDA device needed): build the level hierarchy of p on the

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libst.so")
 
 LEVEL_OPS = ["st_lv_count", "st_lv_get", "st_lv_residual", "st_lv_smooth_S", "st_lv_correct_local",
              "st_lv_correct_apply", "st_lv_restrict", "st_lv_prolong", "st_lv_vcycle", "st_lv_end_values",
-             "st_copy_slabs", "st_zero", "st_sync"]
+             "st_copy_slabs", "st_zero", "st_vec_axpy", "st_vec_sum_blocks", "st_vec_norm2", "st_sync"]
 EXPORTED = ["st_setup", "st_free", "st_set_stream", "st_residual", "st_vcycle", "st_set_graphs", "st_solve",
             "st_solve_host", "st_solve_many_host", "st_info", "st_profile", "st_profile_read", "st_plan", "st_host_matrix",
             *LEVEL_OPS, "st_kernel_variants", "st_variant_name", "st_last_error"]
@@ -96,6 +96,9 @@ def load():
     lib.st_lv_end_values.argtypes = [vp, ci, ci, vp, vp]
     lib.st_copy_slabs.argtypes = [vp, ci, ci, ci, vp, ci, ci, vp, ci, ci, ci]
     lib.st_zero.argtypes = [vp, vp, i64]
+    lib.st_vec_axpy.argtypes = [vp, i64, ctypes.c_double, vp, vp]
+    lib.st_vec_sum_blocks.argtypes = [vp, i64, ci, vp, vp]
+    lib.st_vec_norm2.argtypes = [vp, i64, vp, dp]
     lib.st_sync.argtypes = [vp]
     lib.st_kernel_variants.argtypes = [ctypes.POINTER(ctypes.c_uint64), ci]
     lib.st_variant_name.argtypes = [ci]
@@ -279,7 +282,7 @@ class Solver:
         _check(load().st_solve_host(self._h, _dptr(x), _dptr(f), tol, maxit, ctypes.byref(it), hist))
         return it.value, list(hist[: it.value + 1])
 
-    def solve_many_host(self, xs, fs, tol=1e-8, maxit=100, init_from_x=False):
+    def solve_many_host(self, xs, fs, tol=1e-8, maxit=100, init_from_x=False, history=True):
         """Streaming solves of independent problems (st_solve_many_host): xs (out, or in/out with
         init_from_x) and fs are lists of host float64 arrays in ST layout (page-locked memory,
         e.g. torch's pin_memory().numpy(), lets the copies overlap the solves).  Returns
@@ -291,8 +294,10 @@ class Solver:
         X = (ctypes.POINTER(ctypes.c_double) * n)(*[_dptr(a) for a in xs])
         F = (ctypes.POINTER(ctypes.c_double) * n)(*[_dptr(a) for a in fs])
         it = (ctypes.c_int * max(n, 1))()
-        hist = (ctypes.c_double * max(n * (maxit + 1), 1))()
+        hist = (ctypes.c_double * max(n * (maxit + 1), 1))() if history else None
         _check(load().st_solve_many_host(self._h, n, X, F, 1 if init_from_x else 0, tol, maxit, it, hist))
+        if not history:       # (tol <= 0 then runs exactly maxit cycles without norms)
+            return [it[i] for i in range(n)], None
         return [it[i] for i in range(n)], [list(hist[i * (maxit + 1): i * (maxit + 1) + it[i] + 1]) for i in range(n)]
 
     # ---- level operations (multi-GPU driver: distributed.py) -------------------------
@@ -332,6 +337,23 @@ class Solver:
 
     def zero(self, t):
         _check(load().st_zero(self._h, ctypes.c_void_p(t.data_ptr()), t.numel()))
+
+    def axpy(self, alpha, x, y):
+        """y += alpha x (device tensors of equal size), st_vec_axpy."""
+        assert x.numel() == y.numel()
+        _check(load().st_vec_axpy(self._h, y.numel(), alpha, ctypes.c_void_p(x.data_ptr()),
+                                  ctypes.c_void_p(y.data_ptr())))
+
+    def sum_blocks(self, blocks, nb, out):
+        """out = sum of the first nb rows of blocks (nb x n device tensor), st_vec_sum_blocks."""
+        _check(load().st_vec_sum_blocks(self._h, out.numel(), nb, ctypes.c_void_p(blocks.data_ptr()),
+                                        ctypes.c_void_p(out.data_ptr())))
+
+    def norm2(self, v):
+        """||v||_2^2 of a device tensor, st_vec_norm2."""
+        out = ctypes.c_double()
+        _check(load().st_vec_norm2(self._h, v.numel(), ctypes.c_void_p(v.data_ptr()), ctypes.byref(out)))
+        return out.value
 
     def sync(self):
         _check(load().st_sync(self._h))

@@ -582,7 +582,7 @@ int st_setup(const st_params *p, st_handle **out) {
             D.tau = h->upload(std::vector<double>(H.tau.begin() + b, H.tau.begin() + b + cnt));
             // structured stencil march (stencil.cuh) on class-uniform hex levels whose slab count
             // fills whole warps; env ST_STENCIL=0 keeps the ELL kernels (measurements)
-            if (h->stencil && o.kernel_path == 0 && (Q == 1 || Q == 2) && cnt % (32 / Q) == 0 && H.uniform &&
+            if (h->stencil && o.kernel_path == 0 && (Q == 1 || Q == 2) && cnt % 32 == 0 && H.uniform &&
                 H.mesh.dim == 3) {
                 auto tab = std::make_unique<st::StencilTab>();
                 if (st::build_stencil_tab(H, *tab)) {
@@ -591,6 +591,10 @@ int st_setup(const st_params *p, st_handle **out) {
                     h->st_tabs.push_back(std::move(tab));
                     D.grid.nx = H.mesh.n[0]; D.grid.ny = H.mesh.n[1]; D.grid.nz = H.mesh.n[2];
                     D.grid.Ex = H.mesh.Ex; D.grid.Ey = H.mesh.Ey;
+                    if (P > 1) {
+                        D.st_halo = h->dalloc<double>((size_t)D.n_edges * Q * 2);
+                        ck(cudaMemset(D.st_halo, 0, sizeof(double) * (size_t)D.n_edges * Q * 2), "memset");
+                    }
                 }
             }
             D.space_coarsened = H.space_coarsened;
@@ -771,6 +775,12 @@ int st_solve(st_handle *h, double *x, const double *f, double tol, int maxit, in
     ST_CHECK_ALIGNED(x, f);
     if (h->nranks > 1) return fail(1, "multi-rank handles solve through paper_1911_09548_b200.distributed");
     ST_GUARD({
+        if (tol <= 0.0 && !hist) {
+            // no stopping test and no history requested: exactly maxit V-cycles, no norms
+            for (int it = 0; it < maxit; ++it) run_vcycle(h, x, f);
+            if (iters) *iters = maxit;
+            return 0;
+        }
         const double nf = std::sqrt(norm2_plain(h, f, vec_len(h->dl[0], h->Q)));
         int it = 0;
         for (;; ++it) {
@@ -1061,6 +1071,23 @@ int st_copy_slabs(st_handle *h, int rows, int q, int ns, double *dst, int dS, in
 int st_zero(st_handle *h, double *ptr, int64_t n) {
     if (!h || (!ptr && n)) return fail(1, "null argument");
     ST_GUARD(ck(cudaMemsetAsync(ptr, 0, sizeof(double) * (size_t)n, h->stream), "memset"))
+}
+
+int st_vec_axpy(st_handle *h, int64_t n, double alpha, const double *x, double *y) {
+    if (!h || n < 0 || (n && (!x || !y))) return fail(1, "bad argument");
+    ST_GUARD(if (n) h->run("axpy", 24.0 * n, 1, [&] { st::launch_axpy((st::Stream)h->stream, (size_t)n, alpha, x, y); }))
+}
+
+int st_vec_sum_blocks(st_handle *h, int64_t n, int nb, const double *in, double *out) {
+    if (!h || n < 0 || nb < 0 || (n && (!out || (nb && !in)))) return fail(1, "bad argument");
+    ST_GUARD(if (n) h->run("sum_blocks", 8.0 * n * (nb + 1), 1,
+                           [&] { st::launch_sum_blocks((st::Stream)h->stream, (size_t)n, nb, in, out); }))
+}
+
+int st_vec_norm2(st_handle *h, int64_t n, const double *v, double *out) {
+    if (!h || n < 0 || !out || (n && !v)) return fail(1, "bad argument");
+    if ((size_t)n > (size_t)h->partial_cap * 256) return fail(1, "vector longer than the handle's level vectors");
+    ST_GUARD(*out = n ? norm2_plain(h, v, (size_t)n) : 0.0)
 }
 
 int st_sync(st_handle *h) {

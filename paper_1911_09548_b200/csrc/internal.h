@@ -122,6 +122,7 @@ struct DevLevel {
     bool use_march = false;
     bool use_stencil = false;       // structured stencil march (stencil.cuh) for residual and sweep
     StencilTab *st_tab = nullptr;   // host copy of the level's stencil table (owned by the handle)
+    double *st_halo = nullptr;      // multi-rank: [row][q][2] staging of the previous rank's end values
     int lpr_log2 = 5;       // edge kernels: log2(lanes per row); slab chunk = 2 << lpr_log2 (32: measured best)
     Grid3 grid{};
     double *tau = nullptr;
@@ -164,6 +165,7 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
 void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, bool recon, const double *z,
                   const double *r, double *out, double omega_s, double omega);
 void launch_axpy(Stream st, size_t n, double alpha, const double *z, double *x);
+void launch_sum_blocks(Stream st, size_t n, int nb, const double *in, double *out);
 void launch_gtr(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f, const double *prev,
                 double omega_n, double *zn, double *w);
 void launch_node_sweep(Stream st, const DevLevel &L, int Q, const double *z, const double *w, double omega_n,

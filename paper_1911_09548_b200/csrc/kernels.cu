@@ -14,12 +14,16 @@
 //   transfers      R = P^T, P = P_t (x) P_edge                                            l.84, l.93-109
 // The nodal time basis makes Nt = e_0 e_q^T (only time node 0 of slab k sees the
 // end value of slab k-1) and (Ct^{-1} e_0)_q = 1, checked in setup (R2).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
+#include <string>
+#include <vector>
 
 #include "internal.h"
 #include "march.cuh"
@@ -1196,6 +1200,75 @@ static inline int nblocks(long long work) { return (int)((work + kBlock - 1) / k
 static thread_local int g_extra_launches = 0;
 int take_extra_launches() { const int n = g_extra_launches; g_extra_launches = 0; return n; }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link-time libcuda dependency)
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !ptr)
+            throw std::runtime_error("cuTensorMapEncodeTiled not available");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }();
+    return fn;
+}
+
+// 5-D tiled view (slab, b, i, j, z-level) of one edge block of a space-time vector with S slabs and
+// Q time nodes per row; box (bs, bq, bi, bj, 1)
+static void encode_block(CUtensorMap *m, const double *base, int S, int Q, int ni, int nj, int nl, int bs, int bq,
+                         int bi, int bj) {
+    const cuuint64_t rs = (cuuint64_t)Q * S * 8;
+    const cuuint64_t dims[5] = {(cuuint64_t)S, (cuuint64_t)Q, (cuuint64_t)ni, (cuuint64_t)nj, (cuuint64_t)nl};
+    const cuuint64_t str[4] = {(cuuint64_t)S * 8, rs, rs * ni, rs * ni * nj};
+    const cuuint32_t box[5] = {(cuuint32_t)bs, (cuuint32_t)bq, (cuuint32_t)bi, (cuuint32_t)bj, 1};
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    const CUresult r = tmap_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double *>(base), dims, str, box,
+                                      es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed");
+}
+
+// the three edge blocks of vector v (x-, y-, z-edges) with boxes (bs, bq) per block
+static void encode_vector(CUtensorMap *mx, CUtensorMap *my, CUtensorMap *mz, const DevLevel &L, const double *v, int S,
+                          int Q, int bs, int bq) {
+    const Grid3 &G = L.grid;
+    const size_t QS = (size_t)Q * S;
+    encode_block(mx, v, S, Q, G.nx, G.ny + 1, G.nz + 1, bs, bq, kStTI + 1, kStTJ + 2);
+    encode_block(my, v + (size_t)G.Ex * QS, S, Q, G.nx + 1, G.ny, G.nz + 1, bs, bq, kStTI + 2, kStTJ + 1);
+    encode_block(mz, v + (size_t)(G.Ex + G.Ey) * QS, S, Q, G.nx + 1, G.ny + 1, G.nz, bs, bq, kStTI + 2, kStTJ + 2);
+}
+
+template <int Q>
+static void stencil_maps(const DevLevel &L, const double *v, bool coupling, const double *halo, StMaps &m) {
+    encode_vector(&m.x, &m.y, &m.z, L, v, L.S, Q, kStSPW, Q);
+    if (coupling) {
+        encode_vector(&m.px, &m.py, &m.pz, L, v, L.S, Q, 2, 1);
+        if (halo) encode_vector(&m.hx, &m.hy, &m.hz, L, halo, 2, Q, 2, 1);
+        else { m.hx = m.px; m.hy = m.py; m.hz = m.pz; }
+    }
+}
+
+// halo[row][q][1] = prev[row] (the previous rank's end values as slab 1 of a 2-slab vector)
+__global__ void __launch_bounds__(kBlock) k_st_halo(int n, int Q, const double *__restrict__ prev, double *__restrict__ halo) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) halo[(size_t)i * 2 * Q + (Q - 1) * 2 + 1] = prev[i];
+}
+
+// opt the stencil kernels into their dynamic shared memory (once per kernel and process)
+template <class K>
+static void stencil_smem_attr(K kernel, int bytes) {
+    static std::mutex mu;
+    static std::vector<const void *> done;
+    std::lock_guard<std::mutex> lk(mu);
+    const void *key = reinterpret_cast<const void *>(kernel);
+    for (const void *d : done)
+        if (d == key) return;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess)
+        throw std::runtime_error(std::string("stencil smem attribute: ") + cudaGetErrorString(e));
+    done.push_back(key);
+}
+
 static StGeo stencil_geo(const DevLevel &L, int Q) {
     StGeo g{};
     g.nx = L.grid.nx; g.ny = L.grid.ny; g.nz = L.grid.nz; g.Ex = L.grid.Ex; g.Ey = L.grid.Ey;
@@ -1203,13 +1276,13 @@ static StGeo stencil_geo(const DevLevel &L, int Q) {
     g.tiles_i = (g.nx + 1 + kStTI - 1) / kStTI;
     const int tiles_j = (g.ny + 1 + kStTJ - 1) / kStTJ;
     g.n_tiles = g.tiles_i * tiles_j;
-    g.n_chunks = L.S / (32 / Q);
+    g.n_chunks = L.S / kStSPW;
     return g;
 }
 static inline int grid(const StGeo &g) { return g.n_tiles * g.n_chunks; }
 
 bool stencil_applies(const DevLevel &L, int Q) {
-    return L.use_stencil && L.st_tab && (Q == 1 || Q == 2) && L.S % (32 / Q) == 0;
+    return L.use_stencil && L.st_tab && (Q == 1 || Q == 2) && L.S % kStSPW == 0;
 }
 
 
@@ -1307,16 +1380,29 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
         if (prev) note(V_COUPLING_PREV);
         const StGeo g = stencil_geo(L, Q);
         const int nb = grid(g), nt = 32 * kStWarps;
+        const size_t sm = Q == 1 ? sizeof(StSmem<1>) + 128 : sizeof(StSmem<2>) + 128;
+        if (prev) {
+            if (!L.st_halo) throw std::logic_error("stencil halo buffer missing");
+            k_st_halo<<<nblocks(L.n_edges), kBlock, 0, st>>>(L.n_edges, Q, prev, L.st_halo);
+            ++g_extra_launches;
+        }
+        const int hp = prev ? 1 : 0;
         ST_DISPATCH_Q12(Q, {
+            StMaps maps;
+            stencil_maps<QQ>(L, x, g.n_chunks > 1 || prev, prev ? L.st_halo : nullptr, maps);
+            auto launch = [&](auto kern) {
+                stencil_smem_attr(kern, (int)sm);
+                kern<<<nb, nt, sm, st>>>(g, *L.st_tab, maps, hp, L.tau, f, r, z, omega_s, kt, partial);
+            };
             if (partial) {
-                if (r) k_st_residual<QQ, true, false, true><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, x, f, prev, r, z, omega_s, kt, partial);
-                else k_st_residual<QQ, false, false, true><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, x, f, prev, r, z, omega_s, kt, partial);
+                if (r) launch(k_st_residual<QQ, true, false, true>);
+                else launch(k_st_residual<QQ, false, false, true>);
             } else if (r && z) {
-                k_st_residual<QQ, true, true, false><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, x, f, prev, r, z, omega_s, kt, partial);
+                launch(k_st_residual<QQ, true, true, false>);
             } else if (z) {
-                k_st_residual<QQ, false, true, false><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, x, f, prev, r, z, omega_s, kt, partial);
+                launch(k_st_residual<QQ, false, true, false>);
             } else {
-                k_st_residual<QQ, true, false, false><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, x, f, prev, r, z, omega_s, kt, partial);
+                launch(k_st_residual<QQ, true, false, false>);
             }
         });
         return nb;
@@ -1374,11 +1460,18 @@ void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, 
         note(V_STENCIL_SWEEP);
         const StGeo g = stencil_geo(L, Q);
         const int nb = grid(g), nt = 32 * kStWarps;
+        const size_t sm = Q == 1 ? sizeof(StSmem<1>) + 128 : sizeof(StSmem<2>) + 128;
         ST_DISPATCH_Q12(Q, {
-            if (last && recon) k_st_sweep<QQ, true, true><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, z, r, out, omega_s, omega, kt);
-            else if (last) k_st_sweep<QQ, true, false><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, z, r, out, omega_s, omega, kt);
-            else if (recon) k_st_sweep<QQ, false, true><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, z, r, out, omega_s, omega, kt);
-            else k_st_sweep<QQ, false, false><<<nb, nt, 0, st>>>(g, *L.st_tab, L.tau, z, r, out, omega_s, omega, kt);
+            StMaps maps;
+            stencil_maps<QQ>(L, z, false, nullptr, maps);
+            auto launch = [&](auto kern) {
+                stencil_smem_attr(kern, (int)sm);
+                kern<<<nb, nt, sm, st>>>(g, *L.st_tab, maps, L.tau, r, out, omega_s, omega, kt);
+            };
+            if (last && recon) launch(k_st_sweep<QQ, true, true>);
+            else if (last) launch(k_st_sweep<QQ, true, false>);
+            else if (recon) launch(k_st_sweep<QQ, false, true>);
+            else launch(k_st_sweep<QQ, false, false>);
         });
         return;
     }
@@ -1413,6 +1506,20 @@ void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, 
         else if (recon) k_sweep<QQ, SP, WM_, WK_, false, true, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
         else k_sweep<QQ, SP, WM_, WK_, false, false, DI_><<<g, kBlock, 0, st>>>(m, L.M, MK, L.tau, L.dM, L.dK, z, r, out, omega_s, omega, kt);
     })));
+}
+
+// out[i] = sum_{b < nb} in[b n + i], blocks added in rank order (the Sigma_t carry of R2)
+__global__ void __launch_bounds__(kBlock) k_sum_blocks(size_t n, int nb, const double *__restrict__ in,
+                                                       double *__restrict__ out) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = 0.0;
+    for (int b = 0; b < nb; ++b) acc += in[(size_t)b * n + i];
+    out[i] = acc;
+}
+
+void launch_sum_blocks(Stream st, size_t n, int nb, const double *in, double *out) {
+    if (n) k_sum_blocks<<<nblocks((long long)n), kBlock, 0, st>>>(n, nb, in, out);
 }
 
 void launch_axpy(Stream st, size_t n, double alpha, const double *z, double *x) {

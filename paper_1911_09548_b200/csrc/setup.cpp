@@ -683,13 +683,21 @@ bool build_stencil_tab(const HostLevel &L, StencilTab &tab) {
             has[sl] = true;
             row[sl] = make_double2(mv, kv);
         }
+        // the first row of a class is its representative; every other row must agree with it to a
+        // few ulps of the row's scale (cells of a uniform but non-dyadic mesh, e.g. h = 1/3, get
+        // coordinate differences that round differently, so their element matrices differ by ulps)
         double2 *t = tab.c[T][cls];
         if (!seen[T][cls]) {
             seen[T][cls] = true;
             for (int s2 = 0; s2 < kStSlots; ++s2) t[s2] = row[s2];
         } else {
+            double sm = 0.0, sk = 0.0;
+            for (int s2 = 0; s2 < kStSlots; ++s2) { sm = std::max(sm, std::fabs(row[s2].x)); sk = std::max(sk, std::fabs(row[s2].y)); }
+            const double tm = 8.0 * std::nextafter(sm, 2.0 * sm + 1.0) - 8.0 * sm, tk = 8.0 * std::nextafter(sk, 2.0 * sk + 1.0) - 8.0 * sk;
             for (int s2 = 0; s2 < kStSlots; ++s2)
-                if (std::memcmp(&t[s2], &row[s2], sizeof(double2)) != 0) return false;
+                if (std::fabs(t[s2].x - row[s2].x) > tm || std::fabs(t[s2].y - row[s2].y) > tk ||
+                    ((t[s2].x == 0.0) != (row[s2].x == 0.0)) || ((t[s2].y == 0.0) != (row[s2].y == 0.0)))
+                    return false;
         }
     }
     // every nonzero slot of a class must point at an existing edge for every row of the class

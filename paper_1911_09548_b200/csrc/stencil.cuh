@@ -10,22 +10,19 @@
 // every coefficient follows from the structured numbering of include/st.h: no ELL indices at all.
 //
 // Register reuse (the point of this kernel): a warp marches a pencil of nodes (i, j)
-// along z for 16 slabs x 2 time nodes (lane = (slab, time node a)).  At z-level s it loads the 21
-// edges the pencil's rows need from that level (6 x-edges, 6 y-edges, 9 z-edges) ONCE and pushes
-// their contributions into the open row accumulators of levels s-1, s, s+1 (X, Y rows) and s-1, s
-// (Z rows); the rows of level s-1 are then complete and leave through the epilogue.  That is 21
-// vector loads per node and lane instead of 3 x 33 for three ELL rows: 4.7x fewer L1 wavefronts.
-// A CTA is a tile of kStTI x kStTJ pencils of one slab chunk so that the halo edges neighbouring
-// pencils share are L1 hits.
+// along z for 32 slabs (lane = slab; all q+1 time nodes of the slab in the lane).  At z-level s it
+// reads the 21 edges the pencil's rows need from that level (6 x-edges, 6 y-edges, 9 z-edges) ONCE
+// and pushes their contributions into the open row accumulators of levels s-1, s, s+1 (X, Y rows)
+// and s-1, s (Z rows); the rows of level s-1 are then complete and leave through the epilogue:
+// 21 operand reads per node and slab instead of 3 x 33 for three ELL rows, every coefficient load
+// shared by the q+1 time nodes, and the (q+1) x (q+1) time blocks of R1 applied in registers.
+// A CTA is a tile of kStTI x kStTJ pencils of one slab chunk; its z-levels are staged in shared
+// memory by TMA (below), halo included, so neighbouring pencils share every operand fetch.
 //
-// Upwind coupling (residual only): time node 0 of slab k needs (M x_q) of slab k-1; inside a warp
-// that is the m accumulator of the lane (k-1, q), one shuffle.  For the first slab of the warp the
-// march also accumulates (M x_q) of the slab before the chunk from warp-uniform (broadcast) loads of
-// its 15 mass-coupled neighbours per level (or of the previous rank's end values `prev`).
-//
-// Epilogue per row: the lane holds (M x_a, K x_a) of its own time node a; it forms the
-// contributions of x_a to (A x)_b for both b and swaps the partner's share with one shuffle (the
-// (Q x Q) time blocks Ct, Mt of R1 are applied this way, as is the Jacobi block inverse D^{-1}).
+// Upwind coupling (residual only): time node 0 of slab k needs (M x_q) of slab k-1: inside a warp
+// the mass accumulator of lane k-1 (one shuffle); for the first slab of the chunk the march also
+// accumulates (M x_q) of the slab before it from a staged 2-slab box of the 15 mass-coupled
+// neighbours per level (or from the previous rank's end values `prev`, staged the same way).
 #pragma once
 
 struct StGeo {
@@ -35,6 +32,7 @@ struct StGeo {
 
 constexpr int kStTI = 4, kStTJ = 2;            // pencils per CTA (one warp each)
 constexpr int kStWarps = kStTI * kStTJ;
+constexpr int kStSPW = 32;                     // slabs per warp (lane = slab)
 constexpr int kStInterior = 4;                 // class (1, 1): both transverse coordinates inside
 
 template <bool FAST>
@@ -43,127 +41,109 @@ __device__ __forceinline__ double2 st_coef(const StencilTab &tab, int T, int cls
     return tab.c[T][cls][slot];
 }
 
-// open accumulators of the lane's time node a: (M x_a, K x_a) per row type and open level
+// open accumulators (M x_b, K x_b) per row type, open level and time node b
 // (X, Y rows: levels s-1, s, s+1; Z rows: s-1, s); StPrev: M x_q of the slab before the chunk
+template <int Q>
 struct StAcc {
-    double xm[3], xk[3], ym[3], yk[3], zm[2], zk[2];
+    double xm[3][Q], xk[3][Q], ym[3][Q], yk[3][Q], zm[2][Q], zk[2][Q];
 };
 struct StPrev {
     double x[3], y[3], z[2];
 };
 
-// per-pencil row offsets of the 21 in-plane neighbours (clamped into the mesh: a neighbour that
-// does not exist has a zero coefficient in every class that reaches it)
-struct StPencil {
-    int i, j;
-    bool ok;
-    unsigned ox[2][3], oy[3][2], oz[3][3];
-};
-
-__device__ __forceinline__ int st_clamp(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
-
-__device__ __forceinline__ void st_pencil(const StGeo &g, int tile, int warp, StPencil &P) {
-    const int ti = tile % g.tiles_i, tj = tile / g.tiles_i;
-    P.i = ti * kStTI + warp % kStTI;
-    P.j = tj * kStTJ + warp / kStTI;
-    P.ok = P.i <= g.nx && P.j <= g.ny;
-    const int i = P.ok ? P.i : 0, j = P.ok ? P.j : 0;
+// Push the inputs of z-level s into the open rows.  xin[a][b][q]: x-edge (i-1+a, j-1+b, s), time
+// node q; yin: y-edges (i-1+a, j-1+b, s); zin: z-edges (i-1+a, j-1+b, s).  clsX[d] / clsY[d]:
+// class of the X / Y row at level s-1+d, clsZ: class of the pencil's Z rows.
+template <int Q, bool FAST, bool ZIN>
+__device__ __forceinline__ void st_push(const StencilTab &tab, const double (&xin)[2][3][Q],
+                                        const double (&yin)[3][2][Q], const double (&zin)[3][3][Q],
+                                        const int (&clsX)[3], const int (&clsY)[3], int clsZ, StAcc<Q> &A) {
+    // loop order: input outermost, then the open levels d and time nodes q innermost, so that
+    // consecutive FMAs go to independent accumulators (latency of the fp64 pipe)
+    // ---- x-edge inputs xin[a][b] = x-edge (i-1+a, j-1+b)
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int b = 0; b < 3; ++b) P.ox[a][b] = st_clamp(i - 1 + a, 0, g.nx - 1) + g.nx * st_clamp(j - 1 + b, 0, g.ny);
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) P.oy[a][b] = st_clamp(i - 1 + a, 0, g.nx) + (g.nx + 1) * st_clamp(j - 1 + b, 0, g.ny - 1);
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) P.oz[a][b] = st_clamp(i - 1 + a, 0, g.nx) + (g.nx + 1) * st_clamp(j - 1 + b, 0, g.ny);
-}
-
-// element (row, a, k) of a space-time vector at byte row * rowbytes from the lane base
-__device__ __forceinline__ double st_ld(const char *base, unsigned row, unsigned rowbytes) {
-    return __ldg(reinterpret_cast<const double *>(base + (size_t)row * rowbytes));
-}
-
-// Push the inputs of z-level s into the open rows.  xin[a][b]: x-edge (i-1+a, j-1+b, s); yin[a][b]:
-// y-edge (i-1+a, j-1+b, s); zin[a][b]: z-edge (i-1+a, j-1+b, s).  clsX[d] / clsY[d]: class of the
-// X / Y row at level s-1+d, clsZ: class of the pencil's Z rows.
-template <bool FAST, bool ZIN>
-__device__ __forceinline__ void st_push(const StencilTab &tab, const double (&xin)[2][3], const double (&yin)[3][2],
-                                        const double (&zin)[3][3], const int (&clsX)[3], const int (&clsY)[3],
-                                        int clsZ, StAcc &A) {
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        const int o2 = 1 - d;                  // input level s relative to the row level s-1+d
-        // X rows: x-neighbours (i, j-1+b) o = (0, b-1, o2)
-#pragma unroll
         for (int b = 0; b < 3; ++b) {
-            const double2 c = st_coef<FAST>(tab, 0, clsX[d], st_slot(0, 0, 0, b - 1, o2));
-            A.xm[d] = fma(c.x, xin[1][b], A.xm[d]);
-            A.xk[d] = fma(c.y, xin[1][b], A.xk[d]);
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const int o2 = 1 - d;
+                if (a == 1) {                                   // X rows: o = (0, b-1, o2)
+                    const double2 c = st_coef<FAST>(tab, 0, clsX[d], st_slot(0, 0, 0, b - 1, o2));
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        A.xm[d][q] = fma(c.x, xin[a][b][q], A.xm[d][q]);
+                        A.xk[d][q] = fma(c.y, xin[a][b][q], A.xk[d][q]);
+                    }
+                }
+                if (b >= 1) {                                   // Y rows: o = (a-1, b-1, o2)
+                    const double c = st_coef<FAST>(tab, 1, clsY[d], st_slot(1, 0, a - 1, b - 1, o2)).y;
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) A.yk[d][q] = fma(c, xin[a][b][q], A.yk[d][q]);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {                       // Z rows at s-1+e: o = (a-1, b-1, 1-e)
+                const double c = st_coef<FAST>(tab, 2, clsZ, st_slot(2, 0, a - 1, b - 1, 1 - e)).y;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) A.zk[e][q] = fma(c, xin[a][b][q], A.zk[e][q]);
+            }
         }
-        // X rows: y-neighbours (i-1+a, j-1+b), a in {1,2}, b in {0,1}
+    // ---- y-edge inputs yin[a][b] = y-edge (i-1+a, j-1+b)
 #pragma unroll
-        for (int a = 1; a < 3; ++a)
+    for (int a = 0; a < 3; ++a)
 #pragma unroll
-            for (int b = 0; b < 2; ++b)
-                A.xk[d] = fma(st_coef<FAST>(tab, 0, clsX[d], st_slot(0, 1, a - 1, b - 1, o2)).y, yin[a][b], A.xk[d]);
-        // X rows: z-neighbours (i-1+a, j-1+b) with o2 in {-1, 0} (d in {1, 2}), a in {1,2}
-        if (ZIN && d >= 1) {
+        for (int b = 0; b < 2; ++b) {
 #pragma unroll
-            for (int a = 1; a < 3; ++a)
+            for (int d = 0; d < 3; ++d) {
+                const int o2 = 1 - d;
+                if (a >= 1) {                                   // X rows: o = (a-1, b-1, o2)
+                    const double c = st_coef<FAST>(tab, 0, clsX[d], st_slot(0, 1, a - 1, b - 1, o2)).y;
 #pragma unroll
-                for (int b = 0; b < 3; ++b)
-                    A.xk[d] = fma(st_coef<FAST>(tab, 0, clsX[d], st_slot(0, 2, a - 1, b - 1, o2)).y, zin[a][b], A.xk[d]);
+                    for (int q = 0; q < Q; ++q) A.xk[d][q] = fma(c, yin[a][b][q], A.xk[d][q]);
+                }
+                if (b == 1) {                                   // Y rows: o = (a-1, 0, o2)
+                    const double2 c = st_coef<FAST>(tab, 1, clsY[d], st_slot(1, 1, a - 1, 0, o2));
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        A.ym[d][q] = fma(c.x, yin[a][b][q], A.ym[d][q]);
+                        A.yk[d][q] = fma(c.y, yin[a][b][q], A.yk[d][q]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {                       // Z rows: o = (a-1, b-1, 1-e)
+                const double c = st_coef<FAST>(tab, 2, clsZ, st_slot(2, 1, a - 1, b - 1, 1 - e)).y;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) A.zk[e][q] = fma(c, yin[a][b][q], A.zk[e][q]);
+            }
         }
-        // Y rows: x-neighbours (i-1+a, j-1+b), a in {0,1}, b in {1,2}
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-            for (int b = 1; b < 3; ++b)
-                A.yk[d] = fma(st_coef<FAST>(tab, 1, clsY[d], st_slot(1, 0, a - 1, b - 1, o2)).y, xin[a][b], A.yk[d]);
-        // Y rows: y-neighbours (i-1+a, j)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const double2 c = st_coef<FAST>(tab, 1, clsY[d], st_slot(1, 1, a - 1, 0, o2));
-            A.ym[d] = fma(c.x, yin[a][1], A.ym[d]);
-            A.yk[d] = fma(c.y, yin[a][1], A.yk[d]);
-        }
-        // Y rows: z-neighbours (i-1+a, j-1+b), b in {1,2}
-        if (ZIN && d >= 1) {
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 1; b < 3; ++b)
-                    A.yk[d] = fma(st_coef<FAST>(tab, 1, clsY[d], st_slot(1, 2, a - 1, b - 1, o2)).y, zin[a][b], A.yk[d]);
-        }
-    }
-    // Z rows at level s-1+e: x- and y-neighbours at o2 = 1 - e in {0, 1}
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const int o2 = 1 - e;
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b)
-                A.zk[e] = fma(st_coef<FAST>(tab, 2, clsZ, st_slot(2, 0, a - 1, b - 1, o2)).y, xin[a][b], A.zk[e]);
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 2; ++b)
-                A.zk[e] = fma(st_coef<FAST>(tab, 2, clsZ, st_slot(2, 1, a - 1, b - 1, o2)).y, yin[a][b], A.zk[e]);
-    }
-    // Z row at level s: z-neighbours of the same level only
+    // ---- z-edge inputs zin[a][b] = z-edge (i-1+a, j-1+b) from level s to s+1
     if (ZIN) {
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
             for (int b = 0; b < 3; ++b) {
-                const double2 c = st_coef<FAST>(tab, 2, clsZ, st_slot(2, 2, a - 1, b - 1, 0));
-                A.zm[1] = fma(c.x, zin[a][b], A.zm[1]);
-                A.zk[1] = fma(c.y, zin[a][b], A.zk[1]);
+#pragma unroll
+                for (int d = 1; d < 3; ++d) {                   // X, Y rows at s, s+1: o2 = 1 - d
+                    const int o2 = 1 - d;
+                    if (a >= 1) {
+                        const double c = st_coef<FAST>(tab, 0, clsX[d], st_slot(0, 2, a - 1, b - 1, o2)).y;
+#pragma unroll
+                        for (int q = 0; q < Q; ++q) A.xk[d][q] = fma(c, zin[a][b][q], A.xk[d][q]);
+                    }
+                    if (b >= 1) {
+                        const double c = st_coef<FAST>(tab, 1, clsY[d], st_slot(1, 2, a - 1, b - 1, o2)).y;
+#pragma unroll
+                        for (int q = 0; q < Q; ++q) A.yk[d][q] = fma(c, zin[a][b][q], A.yk[d][q]);
+                    }
+                }
+                const double2 c = st_coef<FAST>(tab, 2, clsZ, st_slot(2, 2, a - 1, b - 1, 0));   // Z row at s
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    A.zm[1][q] = fma(c.x, zin[a][b][q], A.zm[1][q]);
+                    A.zk[1][q] = fma(c.y, zin[a][b][q], A.zk[1][q]);
+                }
             }
     }
 }
@@ -192,118 +172,277 @@ __device__ __forceinline__ void st_push_prev(const StencilTab &tab, const double
     }
 }
 
-// Lane context: time node a, slab k, tau_k, and the column a of the time matrices
-// (cm[b] = Ct[b][a], ck[b] = tau_k Mt[b][a]: the contribution of x_a to (A x)_b per unit M x_a, K x_a)
+// ------------------------------------------------------------- TMA staging
+// Each z-level's inputs of the whole CTA tile are staged in shared memory by three 5-D TMA tile
+// loads (cp.async.bulk.tensor, one elected thread, completion on an mbarrier), kStNB levels ahead
+// of the march.  Tensor view of an edge block of a space-time vector (innermost first):
+// (slab, time node, i, j, z-level); box (32, Q, tile i extent, tile j extent, 1) with the tile's
+// one-edge halo.  Out-of-range box elements (mesh boundary, the z-level above the top) are
+// zero-filled by the TMA unit, so the march needs no index clamping: every missing neighbour reads
+// 0 and has a zero coefficient anyway.  The box lands as [j][i][time node][slab]: a warp reads its
+// 21 x (q+1) inputs with conflict-free 8-byte LDS (lane = slab) at compile-time offsets.
+constexpr int kStNB = 3;                                    // staged z-levels in flight
+constexpr int kStBX = (kStTI + 1) * (kStTJ + 2);            // x-edge blocks per level
+constexpr int kStBY = (kStTI + 2) * (kStTJ + 1);
+constexpr int kStBZ = (kStTI + 2) * (kStTJ + 2);
+// the (slab k0-2, k0-1) pair of time node q per block; every TMA destination starts 128-byte aligned
+constexpr int kStPrevPart = 48;                             // doubles: >= 24 blocks x 2, multiple of 16
+constexpr int kStPrevLevel = 3 * kStPrevPart;
+static_assert(kStBX * 2 <= kStPrevPart && kStBY * 2 <= kStPrevPart && kStBZ * 2 <= kStPrevPart, "prev part");
+
+template <int Q>
+struct StCfg {
+    static constexpr int Blk = Q * kStSPW;                              // doubles per edge block
+    static constexpr int Level = (kStBX + kStBY + kStBZ) * Blk;         // doubles per staged level
+    static_assert((kStBX * Blk * 8) % 128 == 0 && (kStBY * Blk * 8) % 128 == 0 && (Level * 8) % 128 == 0,
+                  "TMA destinations must stay 128-byte aligned");
+};
+
+struct StMaps {
+    CUtensorMap x, y, z;            // the input vector's x-, y-, z-edge blocks
+    CUtensorMap px, py, pz;         // the same vector, box = slab pair (k0-2, k0-1) of time node q
+    CUtensorMap hx, hy, hz;         // the previous rank's end values staged as slab 1 of a 2-slab vector
+};
+
+template <int Q>
+struct alignas(128) StSmem {
+    double buf[kStNB][StCfg<Q>::Level];
+    double prev[kStNB][kStPrevLevel];
+    unsigned long long full[kStNB];
+};
+
+__device__ __forceinline__ unsigned st_smem_addr(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void st_mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(st_smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void st_mbar_expect(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(st_smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void st_mbar_wait(unsigned long long *bar, unsigned parity) {
+    const unsigned a = st_smem_addr(bar);
+    unsigned ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void st_tma_5d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4,
+                                          unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(st_smem_addr(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+        "r"(st_smem_addr(bar))
+        : "memory");
+}
+
+// issue the staging of z-level s into buffer s % kStNB (one thread)
+template <int Q, bool PREVM>
+__device__ __forceinline__ void st_stage(const StGeo &g, const StMaps &maps, StSmem<Q> &sm, int s, int i0, int j0,
+                                         int k0) {
+    using C = StCfg<Q>;
+    const int nb = s % kStNB;
+    const bool zin = s < g.nz;
+    constexpr unsigned bx = kStBX * C::Blk * 8, by = kStBY * C::Blk * 8, bz = kStBZ * C::Blk * 8;
+    constexpr unsigned px = kStBX * 16, py = kStBY * 16, pz = kStBZ * 16;
+    unsigned bytes = bx + by + (zin ? bz : 0);
+    if (PREVM) bytes += px + py + (zin ? pz : 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    st_mbar_expect(&sm.full[nb], bytes);
+    double *b = sm.buf[nb];
+    st_tma_5d(b, &maps.x, k0, 0, i0 - 1, j0 - 1, s, &sm.full[nb]);
+    st_tma_5d(b + kStBX * C::Blk, &maps.y, k0, 0, i0 - 1, j0 - 1, s, &sm.full[nb]);
+    if (zin) st_tma_5d(b + (kStBX + kStBY) * C::Blk, &maps.z, k0, 0, i0 - 1, j0 - 1, s, &sm.full[nb]);
+    if (PREVM) {
+        // (M x_q) of the slab before the chunk: slab k0 - 1 of x, or the previous rank's end values
+        double *p = sm.prev[nb];
+        const bool h = k0 == 0;
+        const int c0 = h ? 0 : k0 - 2;
+        st_tma_5d(p, h ? &maps.hx : &maps.px, c0, Q - 1, i0 - 1, j0 - 1, s, &sm.full[nb]);
+        st_tma_5d(p + kStPrevPart, h ? &maps.hy : &maps.py, c0, Q - 1, i0 - 1, j0 - 1, s, &sm.full[nb]);
+        if (zin) st_tma_5d(p + 2 * kStPrevPart, h ? &maps.hz : &maps.pz, c0, Q - 1, i0 - 1, j0 - 1, s, &sm.full[nb]);
+    }
+}
+
+// Lane constants: slab k, tau_k, and per row type T the Jacobi block D = Ct dM + tau_k Mt dK of the
+// interior class and its inverse (R3), row-major (Q x Q)
 template <int Q>
 struct StLane {
-    static constexpr int SPW = 32 / Q;         // slabs per warp
-    int a, k;
-    double t, cm[Q], ck[Q];
+    int k;
+    double t;
+    double tMt[Q * Q];              // tau_k Mt
 };
 
 template <int Q>
 __device__ __forceinline__ void st_lane(const KT &kt, const double *__restrict__ tau, int chunk, StLane<Q> &L) {
-    const int lane = threadIdx.x & 31;
-    L.a = lane % Q;
-    L.k = chunk * StLane<Q>::SPW + lane / Q;
+    L.k = chunk * kStSPW + (threadIdx.x & 31);
     L.t = __ldg(tau + L.k);
 #pragma unroll
-    for (int b = 0; b < Q; ++b) {
-        double c = kt.Ct[b * Q], m = kt.Mt[b * Q];
+    for (int i = 0; i < Q * Q; ++i) L.tMt[i] = L.t * kt.Mt[i];
+}
+
+// D = Ct dm + tau Mt dk and D^{-1} (row-major)
+template <int Q>
+__device__ __forceinline__ void st_block(const KT &kt, const StLane<Q> &L, double dm, double dk, double (&D)[Q * Q],
+                                         double (&Di)[Q * Q]) {
 #pragma unroll
-        for (int a = 1; a < Q; ++a)
-            if (L.a == a) { c = kt.Ct[b * Q + a]; m = kt.Mt[b * Q + a]; }
-        L.cm[b] = c;
-        L.ck[b] = L.t * m;
-    }
-}
-
-// sum over the Q lanes of a slab of their per-b contributions v[b], for the own b = a
-template <int Q>
-__device__ __forceinline__ double st_gather(const StLane<Q> &L, const double (&v)[Q]) {
+    for (int i = 0; i < Q * Q; ++i) D[i] = kt.Ct[i] * dm + L.tMt[i] * dk;
     if constexpr (Q == 1) {
-        return v[0];
+        Di[0] = 1.0 / D[0];
     } else {
-        const double own = L.a ? v[1] : v[0], other = L.a ? v[0] : v[1];
-        return own + __shfl_xor_sync(0xffffffffu, other, 1);
+        const double inv = 1.0 / (D[0] * D[3] - D[1] * D[2]);
+        Di[0] = D[3] * inv; Di[1] = -D[1] * inv; Di[2] = -D[2] * inv; Di[3] = D[0] * inv;
     }
 }
 
-// column a of the Jacobi block D = Ct dm + tau Mt dk and of its inverse (R3)
+// per-CTA table of the interior-class blocks: [T][D..., D^{-1}...][lane]
 template <int Q>
-__device__ __forceinline__ void st_block(const KT &kt, const StLane<Q> &L, double dm, double dk, double (&Dcol)[Q],
-                                         double (&Icol)[Q]) {
-    if constexpr (Q == 1) {
-        Dcol[0] = kt.Ct[0] * dm + L.t * kt.Mt[0] * dk;
-        Icol[0] = 1.0 / Dcol[0];
-    } else {
-        const double d00 = kt.Ct[0] * dm + L.t * kt.Mt[0] * dk, d01 = kt.Ct[1] * dm + L.t * kt.Mt[1] * dk;
-        const double d10 = kt.Ct[2] * dm + L.t * kt.Mt[2] * dk, d11 = kt.Ct[3] * dm + L.t * kt.Mt[3] * dk;
-        const double inv = 1.0 / (d00 * d11 - d01 * d10);
-        Dcol[0] = L.a ? d01 : d00;
-        Dcol[1] = L.a ? d11 : d10;
-        Icol[0] = (L.a ? -d01 : d11) * inv;
-        Icol[1] = (L.a ? d00 : -d10) * inv;
+struct StBlockTab {
+    double v[3][2 * Q * Q][32];
+};
+
+template <int Q>
+__device__ __forceinline__ void st_block_table(const StencilTab &tab, const KT &kt, const StLane<Q> &L,
+                                               StBlockTab<Q> &bt) {
+    if ((threadIdx.x >> 5) == 0) {
+#pragma unroll
+        for (int T = 0; T < 3; ++T) {
+            const double2 dd = tab.c[T][kStInterior][st_slot(T, T, 0, 0, 0)];
+            double D[Q * Q], Di[Q * Q];
+            st_block<Q>(kt, L, dd.x, dd.y, D, Di);
+#pragma unroll
+            for (int i = 0; i < Q * Q; ++i) { bt.v[T][i][threadIdx.x] = D[i]; bt.v[T][Q * Q + i][threadIdx.x] = Di[i]; }
+        }
     }
 }
 
-// the march over one pencil; Op supplies pre(T, row) (own-row loads of the rows that complete at
-// this step, issued before the step's gathers) and emit<FAST>(T, row, cls, m, k, mprev)
+template <int Q, bool FAST>
+__device__ __forceinline__ void st_row_block(const StencilTab &tab, const KT &kt, const StLane<Q> &L,
+                                             const StBlockTab<Q> &bt, int T, int cls, double (&D)[Q * Q],
+                                             double (&Di)[Q * Q]) {
+    if (FAST) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int i = 0; i < Q * Q; ++i) { D[i] = bt.v[T][i][lane]; Di[i] = bt.v[T][Q * Q + i][lane]; }
+    } else {
+        const double2 dd = st_coef<false>(tab, T, cls, st_slot(T, T, 0, 0, 0));
+        st_block<Q>(kt, L, dd.x, dd.y, D, Di);
+    }
+}
+
+// (A x)_b = sum_a Ct[b][a] (M x_a) + tau Mt[b][a] (K x_a)   (PAPER.md l.51-77 with the R1 blocks)
+template <int Q>
+__device__ __forceinline__ void st_time(const KT &kt, const StLane<Q> &L, const double (&m)[Q], const double (&k)[Q],
+                                        double (&ax)[Q]) {
+#pragma unroll
+    for (int b = 0; b < Q; ++b) {
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < Q; ++a) acc = fma(kt.Ct[b * Q + a], m[a], fma(L.tMt[b * Q + a], k[a], acc));
+        ax[b] = acc;
+    }
+}
+
+// The march of one CTA tile (one pencil per warp) over all z-levels.  Op supplies
+// pre(T, row, own) (own-row values of the rows completing at this step; own = the staged block of
+// the row at its level) and emit<FAST>(T, row, cls, m[Q], k[Q], mprev); every warp reaches every
+// barrier (also warps whose pencil lies outside the mesh).
 template <int Q, bool PREVM, class Op>
-__device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, const StPencil &P, const char *base,
-                                         unsigned rowbytes, const char *pbase, unsigned prowbytes, Op &op) {
-    StAcc A;
+__device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, const StMaps &maps, StSmem<Q> &sm,
+                                         int tile, int chunk, Op &op) {
+    using C = StCfg<Q>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ti = tile % g.tiles_i, tj = tile / g.tiles_i;
+    const int i0 = ti * kStTI, j0 = tj * kStTJ;
+    const int wi = warp % kStTI, wj = warp / kStTI;
+    const int i = i0 + wi, j = j0 + wj;
+    const bool ok = i <= g.nx && j <= g.ny;
+    const int k0 = chunk * kStSPW;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int b = 0; b < kStNB; ++b) st_mbar_init(&sm.full[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < kStNB && s <= g.nz; ++s) st_stage<Q, PREVM>(g, maps, sm, s, i0, j0, k0);
+    StAcc<Q> A;
     StPrev B;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) { A.xm[d] = A.xk[d] = A.ym[d] = A.yk[d] = 0.0; B.x[d] = B.y[d] = 0.0; }
-    A.zm[0] = A.zk[0] = A.zm[1] = A.zk[1] = 0.0;
+    for (int d = 0; d < 3; ++d) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) A.xm[d][q] = A.xk[d][q] = A.ym[d][q] = A.yk[d][q] = 0.0;
+        B.x[d] = B.y[d] = 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) A.zm[0][q] = A.zk[0][q] = A.zm[1][q] = A.zk[1][q] = 0.0;
     B.z[0] = B.z[1] = 0.0;
-    const int i = P.i, j = P.j;
     const int ci = st_cls(i, g.nx), cj = st_cls(j, g.ny);
     const bool inner_pencil = ci == 1 && cj == 1;
     const int clsZ = 3 * ci + cj;
-    const unsigned px_step = (unsigned)(g.nx * (g.ny + 1)), py_step = (unsigned)((g.nx + 1) * g.ny);
-    const unsigned pz_step = (unsigned)((g.nx + 1) * (g.ny + 1));
+    // the warp's block offsets inside a staged level (doubles)
+    const int ox = (wj * (kStTI + 1) + wi) * C::Blk + lane;
+    const int oy = kStBX * C::Blk + (wj * (kStTI + 2) + wi) * C::Blk + lane;
+    const int oz = (kStBX + kStBY) * C::Blk + (wj * (kStTI + 2) + wi) * C::Blk + lane;
+    const int pox = (wj * (kStTI + 1) + wi) * 2 + 1, poy = kStPrevPart + (wj * (kStTI + 2) + wi) * 2 + 1;
+    const int poz = 2 * kStPrevPart + (wj * (kStTI + 2) + wi) * 2 + 1;
     for (int s = 0; s <= g.nz + 1; ++s) {
         const int l = s - 1;                   // level of the rows that complete at this step
         const unsigned rX = (unsigned)(i + g.nx * (j + (g.ny + 1) * l));
         const unsigned rY = (unsigned)(g.Ex + i + (g.nx + 1) * (j + g.ny * l));
         const unsigned rZ = (unsigned)(g.Ex + g.Ey + i + (g.nx + 1) * (j + (g.ny + 1) * l));
-        const bool eX = s >= 1 && i < g.nx, eY = s >= 1 && j < g.ny, eZ = s >= 1 && l < g.nz;
-        if (eX) op.pre(0, rX);
-        if (eY) op.pre(1, rY);
-        if (eZ) op.pre(2, rZ);
+        const bool eX = ok && s >= 1 && i < g.nx, eY = ok && s >= 1 && j < g.ny, eZ = ok && s >= 1 && l < g.nz;
+        const double *lb = sm.buf[(s + kStNB - 1) % kStNB];         // level s-1 (own values)
+        if (eX) op.pre(0, rX, lb + ox + C::Blk * ((kStTI + 1) + 1));
+        if (eY) op.pre(1, rY, lb + oy + C::Blk * ((kStTI + 2) + 1));
+        if (eZ) op.pre(2, rZ, lb + oz + C::Blk * ((kStTI + 2) + 1));
         const bool fast = inner_pencil && s >= 2 && s <= g.nz - 2;
         if (s <= g.nz) {
-            const unsigned bx = px_step * s, by = g.Ex + py_step * s, bz = g.Ex + g.Ey + pz_step * s;
-            double xin[2][3], yin[3][2], zin[3][3];
+            const int nb = s % kStNB;
+            st_mbar_wait(&sm.full[nb], (unsigned)((s / kStNB) & 1));
+            const double *bb = sm.buf[nb];
+            double xin[2][3][Q], yin[3][2][Q], zin[3][3][Q];
 #pragma unroll
             for (int a = 0; a < 2; ++a)
 #pragma unroll
-                for (int b = 0; b < 3; ++b) xin[a][b] = st_ld(base, bx + P.ox[a][b], rowbytes);
+                for (int b = 0; b < 3; ++b)
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) xin[a][b][q] = bb[ox + (b * (kStTI + 1) + a) * C::Blk + q * kStSPW];
 #pragma unroll
             for (int a = 0; a < 3; ++a)
 #pragma unroll
-                for (int b = 0; b < 2; ++b) yin[a][b] = st_ld(base, by + P.oy[a][b], rowbytes);
+                for (int b = 0; b < 2; ++b)
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) yin[a][b][q] = bb[oy + (b * (kStTI + 2) + a) * C::Blk + q * kStSPW];
             const bool zin_ok = s < g.nz;
 #pragma unroll
             for (int a = 0; a < 3; ++a)
 #pragma unroll
-                for (int b = 0; b < 3; ++b) zin[a][b] = zin_ok ? st_ld(base, bz + P.oz[a][b], rowbytes) : 0.0;
+                for (int b = 0; b < 3; ++b)
+#pragma unroll
+                    for (int q = 0; q < Q; ++q)
+                        zin[a][b][q] = zin_ok ? bb[oz + (b * (kStTI + 2) + a) * C::Blk + q * kStSPW] : 0.0;
             double xp[3], yp[3], zp[3][3];
             if (PREVM) {
+                const double *pb = sm.prev[nb];
 #pragma unroll
-                for (int b = 0; b < 3; ++b) xp[b] = st_ld(pbase, bx + P.ox[1][b], prowbytes);
+                for (int b = 0; b < 3; ++b) xp[b] = pb[pox + (b * (kStTI + 1) + 1) * 2];
 #pragma unroll
-                for (int a = 0; a < 3; ++a) yp[a] = st_ld(pbase, by + P.oy[a][1], prowbytes);
+                for (int a = 0; a < 3; ++a) yp[a] = pb[poy + ((kStTI + 2) + a) * 2];
 #pragma unroll
                 for (int a = 0; a < 3; ++a)
 #pragma unroll
-                    for (int b = 0; b < 3; ++b) zp[a][b] = zin_ok ? st_ld(pbase, bz + P.oz[a][b], prowbytes) : 0.0;
+                    for (int b = 0; b < 3; ++b) zp[a][b] = zin_ok ? pb[poz + (b * (kStTI + 2) + a) * 2] : 0.0;
             }
             if (fast) {
                 const int dummy[3] = {0, 0, 0};
-                st_push<true, true>(tab, xin, yin, zin, dummy, dummy, clsZ, A);
+                st_push<Q, true, true>(tab, xin, yin, zin, dummy, dummy, clsZ, A);
                 if (PREVM) st_push_prev<true, true>(tab, xp, yp, zp, dummy, dummy, clsZ, B);
             } else {
                 int clsX[3], clsY[3];
@@ -314,10 +453,10 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
                     clsY[d] = 3 * ci + cl;
                 }
                 if (zin_ok) {
-                    st_push<false, true>(tab, xin, yin, zin, clsX, clsY, clsZ, A);
+                    st_push<Q, false, true>(tab, xin, yin, zin, clsX, clsY, clsZ, A);
                     if (PREVM) st_push_prev<false, true>(tab, xp, yp, zp, clsX, clsY, clsZ, B);
                 } else {
-                    st_push<false, false>(tab, xin, yin, zin, clsX, clsY, clsZ, A);
+                    st_push<Q, false, false>(tab, xin, yin, zin, clsX, clsY, clsZ, A);
                     if (PREVM) st_push_prev<false, false>(tab, xp, yp, zp, clsX, clsY, clsZ, B);
                 }
             }
@@ -334,21 +473,35 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
                 if (eZ) op.template emit<false>(2, rZ, clsZ, A.zm[0], A.zk[0], B.z[0]);
             }
         }
-        A.xm[0] = A.xm[1]; A.xm[1] = A.xm[2]; A.xm[2] = 0.0;
-        A.xk[0] = A.xk[1]; A.xk[1] = A.xk[2]; A.xk[2] = 0.0;
-        A.ym[0] = A.ym[1]; A.ym[1] = A.ym[2]; A.ym[2] = 0.0;
-        A.yk[0] = A.yk[1]; A.yk[1] = A.yk[2]; A.yk[2] = 0.0;
-        A.zm[0] = A.zm[1]; A.zm[1] = 0.0;
-        A.zk[0] = A.zk[1]; A.zk[1] = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            A.xm[0][q] = A.xm[1][q]; A.xm[1][q] = A.xm[2][q]; A.xm[2][q] = 0.0;
+            A.xk[0][q] = A.xk[1][q]; A.xk[1][q] = A.xk[2][q]; A.xk[2][q] = 0.0;
+            A.ym[0][q] = A.ym[1][q]; A.ym[1][q] = A.ym[2][q]; A.ym[2][q] = 0.0;
+            A.yk[0][q] = A.yk[1][q]; A.yk[1][q] = A.yk[2][q]; A.yk[2][q] = 0.0;
+            A.zm[0][q] = A.zm[1][q]; A.zm[1][q] = 0.0;
+            A.zk[0][q] = A.zk[1][q]; A.zk[1][q] = 0.0;
+        }
         if (PREVM) {
             B.x[0] = B.x[1]; B.x[1] = B.x[2]; B.x[2] = 0.0;
             B.y[0] = B.y[1]; B.y[1] = B.y[2]; B.y[2] = 0.0;
             B.z[0] = B.z[1]; B.z[1] = 0.0;
         }
+        // every warp is done with level s-1 (own values) and level s: refill the buffer of
+        // level s-1 with level s-1+kStNB
+        __syncthreads();
+        if (threadIdx.x == 0 && s >= 1 && s - 1 + kStNB <= g.nz)
+            st_stage<Q, PREVM>(g, maps, sm, s - 1 + kStNB, i0, j0, k0);
     }
 }
 
 // ------------------------------------------------------------------ kernels
+// element (row, b, k) of a space-time vector: row * rowbytes + b * S * 8 + k * 8 from the base
+struct StRow {
+    size_t off;                     // row * rowbytes + k * 8
+    size_t bstride;                 // S * 8
+};
+
 // Residual epilogue: r = f - L x; z = omega_s D^{-1} r (the first
 // block-Jacobi sweep of Eq. (2) from zero, l.79-82); |r|^2 partials.
 template <int Q, bool R_OUT, bool Z_OUT, bool NORM>
@@ -356,66 +509,70 @@ struct StResOp {
     const StencilTab &tab;
     const KT &kt;
     const StLane<Q> &L;
-    const char *fb;                 // f + (a*S + k) elements, in bytes
+    const StBlockTab<Q> &bt;
+    const char *fb;                 // f + k elements, in bytes
     char *rb, *zb;
     unsigned rowbytes;
+    size_t bstride;
     double omega_s;
     bool first;                     // lane of the chunk's first slab
     double nrm;
-    double fv[3];
-    __device__ __forceinline__ void pre(int T, unsigned row) { fv[T] = st_ld(fb, row, rowbytes); }
+    double fv[3][Q];
+    __device__ __forceinline__ void pre(int T, unsigned row, const double *) {
+        const char *p = fb + (size_t)row * rowbytes;
+#pragma unroll
+        for (int b = 0; b < Q; ++b) fv[T][b] = __ldg(reinterpret_cast<const double *>(p + b * bstride));
+    }
     template <bool FAST>
-    __device__ __forceinline__ void emit(int T, unsigned row, int cls, double m, double k, double mprev) {
-        double u[Q];
+    __device__ __forceinline__ void emit(int T, unsigned row, int cls, const double (&m)[Q], const double (&k)[Q],
+                                         double mprev) {
+        double ax[Q], rr[Q];
+        st_time<Q>(kt, L, m, k, ax);
+        // upwind coupling on time node 0: (M x_q)(k-1), lane k-1's mass accumulator of node q
+        const double up = __shfl_up_sync(0xffffffffu, m[Q - 1], 1);
+        const double mp = first ? mprev : up;
 #pragma unroll
-        for (int b = 0; b < Q; ++b) u[b] = L.cm[b] * m + L.ck[b] * k;
-        const double ax = st_gather<Q>(L, u);
-        // upwind coupling on time node 0: (M x_q)(k-1) from lane (k-1, q), right before this lane
-        const double up = __shfl_up_sync(0xffffffffu, m, 1);
-        const double mp = L.a != 0 ? 0.0 : (first ? mprev : up);
-        const double rr = fv[T] - ax + mp;
+        for (int b = 0; b < Q; ++b) rr[b] = fv[T][b] - ax[b] + (b == 0 ? mp : 0.0);
         const size_t off = (size_t)row * rowbytes;
-        if (R_OUT) *reinterpret_cast<double *>(rb + off) = rr;
-        if (Z_OUT) {
-            const double2 dd = st_coef<FAST>(tab, T, cls, st_slot(T, T, 0, 0, 0));
-            double Dc[Q], Ic[Q], v[Q];
-            st_block<Q>(kt, L, dd.x, dd.y, Dc, Ic);
+        if (R_OUT)
 #pragma unroll
-            for (int b = 0; b < Q; ++b) v[b] = Ic[b] * rr;
-            *reinterpret_cast<double *>(zb + off) = omega_s * st_gather<Q>(L, v);
+            for (int b = 0; b < Q; ++b) *reinterpret_cast<double *>(rb + off + b * bstride) = rr[b];
+        if (Z_OUT) {
+            double D[Q * Q], Di[Q * Q];
+            st_row_block<Q, FAST>(tab, kt, L, bt, T, cls, D, Di);
+#pragma unroll
+            for (int b = 0; b < Q; ++b) {
+                double acc = 0.0;
+#pragma unroll
+                for (int a = 0; a < Q; ++a) acc = fma(Di[b * Q + a], rr[a], acc);
+                *reinterpret_cast<double *>(zb + off + b * bstride) = omega_s * acc;
+            }
         }
-        if (NORM) nrm = fma(rr, rr, nrm);
+        if (NORM)
+#pragma unroll
+            for (int b = 0; b < Q; ++b) nrm = fma(rr[b], rr[b], nrm);
     }
 };
 
 template <int Q, bool R_OUT, bool Z_OUT, bool NORM>
-__global__ void __launch_bounds__(32 * kStWarps, 2)
-k_st_residual(StGeo g, const __grid_constant__ StencilTab tab, const double *__restrict__ tau,
-              const double *__restrict__ x, const double *__restrict__ f, const double *__restrict__ prev,
-              double *__restrict__ r, double *__restrict__ z, double omega_s, KT kt, double *__restrict__ partial) {
+__global__ void __launch_bounds__(32 * kStWarps, 1)
+k_st_residual(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constant__ StMaps maps, int has_prev,
+              const double *__restrict__ tau, const double *__restrict__ f, double *__restrict__ r,
+              double *__restrict__ z, double omega_s, KT kt, double *__restrict__ partial) {
+    extern __shared__ __align__(128) unsigned char st_dyn[];
+    StSmem<Q> &sm = *reinterpret_cast<StSmem<Q> *>(st_dyn + ((128u - (st_smem_addr(st_dyn) & 127u)) & 127u));
+    __shared__ StBlockTab<Q> bt;
     const int chunk = blockIdx.x / g.n_tiles, tile = blockIdx.x - chunk * g.n_tiles;
     StLane<Q> L;
     st_lane<Q>(kt, tau, chunk, L);
-    StPencil P;
-    st_pencil(g, tile, threadIdx.x >> 5, P);
+    st_block_table<Q>(tab, kt, L, bt);            // (the march's first barrier publishes it)
     const unsigned rowbytes = (unsigned)(8u * Q * g.S);
-    const size_t lane_off = ((size_t)L.a * g.S + L.k) * 8;
-    StResOp<Q, R_OUT, Z_OUT, NORM> op{tab, kt, L, reinterpret_cast<const char *>(f) + lane_off,
+    const size_t lane_off = (size_t)L.k * 8;
+    StResOp<Q, R_OUT, Z_OUT, NORM> op{tab, kt, L, bt, reinterpret_cast<const char *>(f) + lane_off,
                                       reinterpret_cast<char *>(r) + lane_off, reinterpret_cast<char *>(z) + lane_off,
-                                      rowbytes, omega_s, (threadIdx.x & 31) < Q, 0.0, {0.0, 0.0, 0.0}};
-    if (P.ok) {
-        const char *base = reinterpret_cast<const char *>(x) + lane_off;
-        const int k0 = chunk * StLane<Q>::SPW;
-        if (k0 > 0) {
-            // warp-uniform (broadcast) loads of x_q at slab k0 - 1
-            const char *pb = reinterpret_cast<const char *>(x) + ((size_t)(Q - 1) * g.S + k0 - 1) * 8;
-            st_march<Q, true>(g, tab, P, base, rowbytes, pb, rowbytes, op);
-        } else if (prev) {
-            st_march<Q, true>(g, tab, P, base, rowbytes, reinterpret_cast<const char *>(prev), 8u, op);
-        } else {
-            st_march<Q, false>(g, tab, P, base, rowbytes, nullptr, 0u, op);
-        }
-    }
+                                      rowbytes, (size_t)g.S * 8, omega_s, (threadIdx.x & 31) == 0, 0.0, {}};
+    if (chunk > 0 || has_prev) st_march<Q, true>(g, tab, maps, sm, tile, chunk, op);
+    else st_march<Q, false>(g, tab, maps, sm, tile, chunk, op);
     if (NORM) {
         __shared__ double sh[kStWarps];
         const double s = block_reduce_sum(op.nrm, sh);
@@ -430,50 +587,71 @@ struct StSweepOp {
     const StencilTab &tab;
     const KT &kt;
     const StLane<Q> &L;
-    const char *zb, *rb;
+    const StBlockTab<Q> &bt;
+    const char *rb;
     char *ob;
     unsigned rowbytes;
+    size_t bstride;
     double omega_s, omega;
-    double zv[3], rv[3], xv[3];
-    __device__ __forceinline__ void pre(int T, unsigned row) {
+    double zv[3][Q], rv[3][Q], xv[3][Q];
+    __device__ __forceinline__ void pre(int T, unsigned row, const double *own) {
         const size_t off = (size_t)row * rowbytes;
-        zv[T] = __ldg(reinterpret_cast<const double *>(zb + off));
-        if (!RECON) rv[T] = __ldg(reinterpret_cast<const double *>(rb + off));
-        if (LAST) xv[T] = *reinterpret_cast<const double *>(ob + off);
+#pragma unroll
+        for (int b = 0; b < Q; ++b) {
+            zv[T][b] = own[b * kStSPW];                     // staged z of the row (level s-1)
+            if (!RECON) rv[T][b] = __ldg(reinterpret_cast<const double *>(rb + off + b * bstride));
+            if (LAST) xv[T][b] = *reinterpret_cast<const double *>(ob + off + b * bstride);
+        }
     }
     template <bool FAST>
-    __device__ __forceinline__ void emit(int T, unsigned row, int cls, double m, double k, double) {
-        const double2 dd = st_coef<FAST>(tab, T, cls, st_slot(T, T, 0, 0, 0));
-        double Dc[Q], Ic[Q], c[Q], v[Q];
-        st_block<Q>(kt, L, dd.x, dd.y, Dc, Ic);
+    __device__ __forceinline__ void emit(int T, unsigned row, int cls, const double (&m)[Q], const double (&k)[Q],
+                                         double) {
+        double D[Q * Q], Di[Q * Q], az[Q], d[Q];
+        st_row_block<Q, FAST>(tab, kt, L, bt, T, cls, D, Di);
+        st_time<Q>(kt, L, m, k, az);
         // d = r - A z, with r = D z / omega_s (RECON) or read
 #pragma unroll
-        for (int b = 0; b < Q; ++b) c[b] = (RECON ? Dc[b] * zv[T] / omega_s : 0.0) - (L.cm[b] * m + L.ck[b] * k);
-        const double d = st_gather<Q>(L, c) + (RECON ? 0.0 : rv[T]);
+        for (int b = 0; b < Q; ++b) {
+            double rb_ = 0.0;
+            if (RECON) {
 #pragma unroll
-        for (int b = 0; b < Q; ++b) v[b] = Ic[b] * d;
-        const double res = zv[T] + omega_s * st_gather<Q>(L, v);
-        double *o = reinterpret_cast<double *>(ob + (size_t)row * rowbytes);
-        if (LAST) *o = xv[T] + omega * res;
-        else *o = res;
+                for (int a = 0; a < Q; ++a) rb_ = fma(D[b * Q + a], zv[T][a], rb_);
+                rb_ /= omega_s;
+            } else {
+                rb_ = rv[T][b];
+            }
+            d[b] = rb_ - az[b];
+        }
+        const size_t off = (size_t)row * rowbytes;
+#pragma unroll
+        for (int b = 0; b < Q; ++b) {
+            double y = 0.0;
+#pragma unroll
+            for (int a = 0; a < Q; ++a) y = fma(Di[b * Q + a], d[a], y);
+            const double res = zv[T][b] + omega_s * y;
+            double *o = reinterpret_cast<double *>(ob + off + b * bstride);
+            if (LAST) *o = xv[T][b] + omega * res;
+            else *o = res;
+        }
     }
 };
 
 template <int Q, bool LAST, bool RECON>
-__global__ void __launch_bounds__(32 * kStWarps, 2)
-k_st_sweep(StGeo g, const __grid_constant__ StencilTab tab, const double *__restrict__ tau,
-           const double *__restrict__ z, const double *__restrict__ r, double *out, double omega_s, double omega,
+__global__ void __launch_bounds__(32 * kStWarps, 1)
+k_st_sweep(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constant__ StMaps maps,
+           const double *__restrict__ tau, const double *__restrict__ r, double *out, double omega_s, double omega,
            KT kt) {
+    extern __shared__ __align__(128) unsigned char st_dyn[];
+    StSmem<Q> &sm = *reinterpret_cast<StSmem<Q> *>(st_dyn + ((128u - (st_smem_addr(st_dyn) & 127u)) & 127u));
+    __shared__ StBlockTab<Q> bt;
     const int chunk = blockIdx.x / g.n_tiles, tile = blockIdx.x - chunk * g.n_tiles;
     StLane<Q> L;
     st_lane<Q>(kt, tau, chunk, L);
-    StPencil P;
-    st_pencil(g, tile, threadIdx.x >> 5, P);
-    if (!P.ok) return;
+    st_block_table<Q>(tab, kt, L, bt);
     const unsigned rowbytes = (unsigned)(8u * Q * g.S);
-    const size_t lane_off = ((size_t)L.a * g.S + L.k) * 8;
-    StSweepOp<Q, LAST, RECON> op{tab, kt, L, reinterpret_cast<const char *>(z) + lane_off,
-                                 reinterpret_cast<const char *>(r) + lane_off, reinterpret_cast<char *>(out) + lane_off,
-                                 rowbytes, omega_s, omega, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    st_march<Q, false>(g, tab, P, reinterpret_cast<const char *>(z) + lane_off, rowbytes, nullptr, 0u, op);
+    const size_t lane_off = (size_t)L.k * 8;
+    StSweepOp<Q, LAST, RECON> op{tab, kt, L, bt, reinterpret_cast<const char *>(r) + lane_off,
+                                 reinterpret_cast<char *>(out) + lane_off, rowbytes, (size_t)g.S * 8, omega_s, omega,
+                                 {}, {}, {}};
+    st_march<Q, false>(g, tab, maps, sm, tile, chunk, op);
 }

@@ -16,7 +16,9 @@ communication for neighboring time nodes"):
 
 Communication uses torch.distributed (NCCL on GPUs, gloo on CPU in tests/test_distributed.py,
 where the same driver runs with the CPU oracle as backend).  The driver never computes: every
-arithmetic step is a backend call."""
+arithmetic step is a backend call (with GpuOps a libst kernel: level operations, the Sigma_t rank
+carry st_vec_sum_blocks, the coarse-correction add st_vec_axpy, norms st_vec_norm2); torch only
+moves memory (collectives, slab-block copies)."""
 import torch
 import torch.distributed as dist
 
@@ -112,11 +114,11 @@ class DistributedVCycle:
                 tot = self.ops.correct_local(l, x, f, prev)
                 carry = None
                 if self.comm.size > 1:
+                    # Sigma_t across ranks (R2): the end values integrated over the ranks before
+                    # this one, summed by a kernel in rank order
                     tots = self.comm.allgather(tot)
                     if self.comm.rank > 0:
-                        carry = tots[0].clone()
-                        for t in tots[1:self.comm.rank]:
-                            carry += t
+                        carry = self.ops.carry(tots, self.comm.rank)
                 self.ops.correct_apply(l, x, carry)
 
     def residual_norm2(self, x, f):
@@ -124,7 +126,7 @@ class DistributedVCycle:
         return self.comm.allreduce_sum(local, f) if self.comm.size > 1 else local
 
     def norm2(self, f):
-        local = float((f * f).sum())
+        local = self.ops.norm2(f)
         return self.comm.allreduce_sum(local, f) if self.comm.size > 1 else local
 
     def solve(self, x, f, tol=1e-8, maxit=100):
@@ -271,10 +273,18 @@ class GpuOps:
         self.s.zero(t)
 
     def add(self, x, c):
-        x += c
+        self.s.axpy(1.0, c, x)
 
     def assign(self, x, c):
-        x.copy_(c)
+        x.copy_(c)                      # a device copy (no arithmetic)
+
+    def carry(self, tots, rank):
+        out = torch.empty_like(tots[0])
+        self.s.sum_blocks(torch.stack(tots[:rank]), rank, out)
+        return out
+
+    def norm2(self, v):
+        return self.s.norm2(v)
 
     def join_slabs(self, parts):
         L = self._lv(1, 0)

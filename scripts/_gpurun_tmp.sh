@@ -1,4 +1,2 @@
-ST_STENCIL=1 python scripts/diag_precision.py > gpurun_out/r2_f_diag.log 2>&1
-echo "--- ELL" >> gpurun_out/r2_f_diag.log
-ST_STENCIL=0 python scripts/diag_precision.py >> gpurun_out/r2_f_diag.log 2>&1
-cat gpurun_out/r2_f_diag.log
+timeout 1700 python -m pytest tests -m gpu -q -p no:cacheprovider -rf -x > gpurun_out/r2_k_pytest.log 2>&1; echo rc=$? >> gpurun_out/r2_k_pytest.log
+tail -15 gpurun_out/r2_k_pytest.log

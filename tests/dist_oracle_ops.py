@@ -145,6 +145,15 @@ class OracleOps:
     def add(self, x, c):
         x += c
 
+    def carry(self, tots, rank):
+        out = tots[0].clone()
+        for t in tots[1:rank]:
+            out += t
+        return out
+
+    def norm2(self, v):
+        return float((v * v).sum())
+
     def assign(self, x, c):
         x.copy_(c)
 

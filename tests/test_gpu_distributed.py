@@ -71,17 +71,20 @@ def _worker(rank, P, port, name, out, opts=None):
         parts = drv.comm.gather_to_root(x)
         x.zero_()
         it, hist = drv.solve(x, f, tol=1e-10, maxit=5)
+        variants = p.kernel_variants()
+        gathered = [None] * P
+        dist.all_gather_object(gathered, sorted(variants))
         if rank == 0:
-            out.put((torch.cat([q.cpu() for q in parts], dim=2).numpy(), hist))
+            out.put((torch.cat([q.cpu() for q in parts], dim=2).numpy(), hist, gathered))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("name,P,opts", [("c1", 2, {}), ("c4", 2, {}), ("c5", 2, {}), ("c1", 4, {}),
                                          ("c4", 2, {"inner": "mg"}),
-                                         # 16 slabs per rank: the stencil march with the previous
+                                         # 32 slabs per rank: the stencil march with the previous
                                          # rank's end values as the upwind coupling of slab 0
-                                         ("c4_s32", 2, {})])
+                                         ("c4_s64", 2, {})])
 def test_two_ranks_one_gpu(name, P, opts):
     import torch.multiprocessing as mp
     import paper_1911_09548_b200 as p
@@ -93,7 +96,10 @@ def test_two_ranks_one_gpu(name, P, opts):
     procs = [ctx.Process(target=_worker, args=(r, P, port, name, q, opts)) for r in range(P)]
     for pr in procs:
         pr.start()
-    Xd, hist = q.get(timeout=600)
+    Xd, hist, variants = q.get(timeout=600)
+    if name == "c4_s64":
+        # rank 1 ran the stencil residual with rank 0's end values as its upwind coupling
+        assert "stencil/residual" in variants[1] and "coupling/prev" in variants[1], variants
     for pr in procs:
         pr.join(timeout=120)
         assert pr.exitcode == 0

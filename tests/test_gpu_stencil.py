@@ -19,7 +19,8 @@ def uniform_case(n, S, q, sigma=2.0, nu=0.5, lam=1.0):
                               rhs_seed=7)
 
 
-CASES = [((1, 1, 1), 16, 1), ((2, 3, 4), 48, 1), ((4, 2, 6), 32, 1), ((5, 3, 3), 16, 1), ((3, 3, 3), 64, 0),
+# slab counts: multiples of the 32-slab warp chunk (the stencil's applicability condition)
+CASES = [((1, 1, 1), 32, 1), ((2, 3, 4), 64, 1), ((4, 2, 6), 32, 1), ((5, 3, 3), 32, 1), ((3, 3, 3), 64, 0),
          ((6, 4, 2), 32, 0), ((8, 8, 8), 96, 1)]
 
 

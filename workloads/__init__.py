@@ -155,6 +155,6 @@ def small(name):
         "c2_lam10": lambda: c2(10.0, n=16, S=32),
         "c3": lambda: c3(n=8, S=32),
         "c4": lambda: c4(n=8, S=16, tau=1.0 / 64),
-        "c4_s32": lambda: c4(n=8, S=32, tau=1.0 / 64),
+        "c4_s64": lambda: c4(n=8, S=64, tau=1.0 / 64),
         "c5": lambda: c5(n=6, S=32),
     }[name]()
