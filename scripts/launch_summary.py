@@ -35,10 +35,12 @@ def main(csv_path, bench_log, steps):
     print("total %.1f ms = %.1f ms / V-cycle serialised; bench.py (CUDA events, same command without ncu): %.1f ms / V-cycle"
           % (tot, tot / steps, d["ms_per_step"]))
     ev = sum(v["ms"] for v in d["kernels"].values())
-    tags = {"residual": "k_residual", "sweep_update": "k_sweep", "gtr_mass": "k_res_mass", "node_scan": "k_node_scan",
-            "gt": "k_gt<", "g_update": "k_g_update", "prolong": "k_prolong", "restrict": "k_restrict"}
+    tags = {"residual": ("k_residual", "k_st_residual"), "sweep_update": ("k_sweep", "k_st_sweep"),
+            "gtr_mass": ("k_res_mass",), "node_scan": ("k_node_scan",), "gt": ("k_gt<",),
+            "g_update": ("k_g_update",), "prolong": ("k_prolong",), "restrict": ("k_restrict",)}
     print("family shares, ncu / live events: " + ", ".join(
-        "%s %.1f%% / %.1f%%" % (f, 100 * sum(v[1] for k, v in agg.items() if t in k) / tot, 100 * d["kernels"][f]["ms"] / ev)
+        "%s %.1f%% / %.1f%%" % (f, 100 * sum(v[1] for k, v in agg.items() if any(x in k for x in t)) / tot,
+                                100 * d["kernels"][f]["ms"] / ev)
         for f, t in tags.items() if f in d["kernels"]))
 
 
