@@ -591,10 +591,7 @@ int st_setup(const st_params *p, st_handle **out) {
                     h->st_tabs.push_back(std::move(tab));
                     D.grid.nx = H.mesh.n[0]; D.grid.ny = H.mesh.n[1]; D.grid.nz = H.mesh.n[2];
                     D.grid.Ex = H.mesh.Ex; D.grid.Ey = H.mesh.Ey;
-                    if (P > 1) {
-                        D.st_halo = h->dalloc<double>((size_t)D.n_edges * Q * 2);
-                        ck(cudaMemset(D.st_halo, 0, sizeof(double) * (size_t)D.n_edges * Q * 2), "memset");
-                    }
+                    D.st_cpl = h->dalloc<double>((size_t)D.n_edges * (cnt / 32));
                 }
             }
             D.space_coarsened = H.space_coarsened;

@@ -122,7 +122,7 @@ struct DevLevel {
     bool use_march = false;
     bool use_stencil = false;       // structured stencil march (stencil.cuh) for residual and sweep
     StencilTab *st_tab = nullptr;   // host copy of the level's stencil table (owned by the handle)
-    double *st_halo = nullptr;      // multi-rank: [row][q][2] staging of the previous rank's end values
+    double *st_cpl = nullptr;       // [chunk][row] upwind coupling of each 32-slab chunk's first slab
     int lpr_log2 = 5;       // edge kernels: log2(lanes per row); slab chunk = 2 << lpr_log2 (32: measured best)
     Grid3 grid{};
     double *tau = nullptr;

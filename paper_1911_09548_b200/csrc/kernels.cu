@@ -703,7 +703,7 @@ __global__ void __launch_bounds__(kBlock) k_node_sweep(BoxMap m, DevELL Kn, cons
 //   s_k = (Ct^{-1} z2)_q,  e_k = carry + sum_{j<=k} s_j   (lane-local pair + warp inclusive scan)
 //   y_k = Ct^{-1} z2 + g e_{k-1},  g = Ct^{-1} e_0
 // tot (optional) receives the row's e_{S-1} (rank carry for multi-GPU slabs).
-template <int Q, int SPL, int MODE>
+template <int Q, int SPL, int MODE, int KW = 0>
 __global__ void __launch_bounds__(kBlock) k_node_scan(int nodes, int S, DevELL Kn, const double *__restrict__ dN,
                                                       const double *__restrict__ z, const double *__restrict__ w,
                                                       double omega_n, KT kt, const double *__restrict__ carry_in,
@@ -739,7 +739,9 @@ __global__ void __launch_bounds__(kBlock) k_node_scan(int nodes, int S, DevELL K
                 for (int a = 0; a < Q; ++a)
 #pragma unroll
                     for (int j = 0; j < SPL; ++j) kz[a][j] = 0.0;
-                for (int s = 0; s < Kn.width; ++s) {
+                const int kw = KW > 0 ? KW : Kn.width;
+#pragma unroll (KW > 0 ? KW : 1)
+                for (int s = 0; s < kw; ++s) {
                     double v; int c;
                     ld_ent(en + s, v, c);
                     const double *zc = z + (size_t)c * Q * S + k0;
@@ -1228,30 +1230,20 @@ static void encode_block(CUtensorMap *m, const double *base, int S, int Q, int n
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed");
 }
 
-// the three edge blocks of vector v (x-, y-, z-edges) with boxes (bs, bq) per block
+// the three edge blocks of vector v (x-, y-, z-edges) with boxes (bs, bq, tile extents + halo)
+template <class Tl>
 static void encode_vector(CUtensorMap *mx, CUtensorMap *my, CUtensorMap *mz, const DevLevel &L, const double *v, int S,
                           int Q, int bs, int bq) {
     const Grid3 &G = L.grid;
     const size_t QS = (size_t)Q * S;
-    encode_block(mx, v, S, Q, G.nx, G.ny + 1, G.nz + 1, bs, bq, kStTI + 1, kStTJ + 2);
-    encode_block(my, v + (size_t)G.Ex * QS, S, Q, G.nx + 1, G.ny, G.nz + 1, bs, bq, kStTI + 2, kStTJ + 1);
-    encode_block(mz, v + (size_t)(G.Ex + G.Ey) * QS, S, Q, G.nx + 1, G.ny + 1, G.nz, bs, bq, kStTI + 2, kStTJ + 2);
+    encode_block(mx, v, S, Q, G.nx, G.ny + 1, G.nz + 1, bs, bq, Tl::TI + 1, Tl::TJ + 2);
+    encode_block(my, v + (size_t)G.Ex * QS, S, Q, G.nx + 1, G.ny, G.nz + 1, bs, bq, Tl::TI + 2, Tl::TJ + 1);
+    encode_block(mz, v + (size_t)(G.Ex + G.Ey) * QS, S, Q, G.nx + 1, G.ny + 1, G.nz, bs, bq, Tl::TI + 2, Tl::TJ + 2);
 }
 
-template <int Q>
-static void stencil_maps(const DevLevel &L, const double *v, bool coupling, const double *halo, StMaps &m) {
-    encode_vector(&m.x, &m.y, &m.z, L, v, L.S, Q, kStSPW, Q);
-    if (coupling) {
-        encode_vector(&m.px, &m.py, &m.pz, L, v, L.S, Q, 2, 1);
-        if (halo) encode_vector(&m.hx, &m.hy, &m.hz, L, halo, 2, Q, 2, 1);
-        else { m.hx = m.px; m.hy = m.py; m.hz = m.pz; }
-    }
-}
-
-// halo[row][q][1] = prev[row] (the previous rank's end values as slab 1 of a 2-slab vector)
-__global__ void __launch_bounds__(kBlock) k_st_halo(int n, int Q, const double *__restrict__ prev, double *__restrict__ halo) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) halo[(size_t)i * 2 * Q + (Q - 1) * 2 + 1] = prev[i];
+template <int Q, class Tl>
+static void stencil_maps(const DevLevel &L, const double *v, StMaps &m) {
+    encode_vector<Tl>(&m.x, &m.y, &m.z, L, v, L.S, Q, kStSPW, Q);
 }
 
 // opt the stencil kernels into their dynamic shared memory (once per kernel and process)
@@ -1269,12 +1261,13 @@ static void stencil_smem_attr(K kernel, int bytes) {
     done.push_back(key);
 }
 
-static StGeo stencil_geo(const DevLevel &L, int Q) {
+template <class Tl>
+static StGeo stencil_geo(const DevLevel &L) {
     StGeo g{};
     g.nx = L.grid.nx; g.ny = L.grid.ny; g.nz = L.grid.nz; g.Ex = L.grid.Ex; g.Ey = L.grid.Ey;
     g.S = L.S;
-    g.tiles_i = (g.nx + 1 + kStTI - 1) / kStTI;
-    const int tiles_j = (g.ny + 1 + kStTJ - 1) / kStTJ;
+    g.tiles_i = (g.nx + 1 + Tl::TI - 1) / Tl::TI;
+    const int tiles_j = (g.ny + 1 + Tl::TJ - 1) / Tl::TJ;
     g.n_tiles = g.tiles_i * tiles_j;
     g.n_chunks = L.S / kStSPW;
     return g;
@@ -1378,21 +1371,25 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
     if (stencil_applies(L, Q)) {
         note(V_STENCIL_RES);
         if (prev) note(V_COUPLING_PREV);
-        const StGeo g = stencil_geo(L, Q);
-        const int nb = grid(g), nt = 32 * kStWarps;
-        const size_t sm = Q == 1 ? sizeof(StSmem<1>) + 128 : sizeof(StSmem<2>) + 128;
-        if (prev) {
-            if (!L.st_halo) throw std::logic_error("stencil halo buffer missing");
-            k_st_halo<<<nblocks(L.n_edges), kBlock, 0, st>>>(L.n_edges, Q, prev, L.st_halo);
-            ++g_extra_launches;
-        }
-        const int hp = prev ? 1 : 0;
+        using Tl = StTileRes;
+        const StGeo g = stencil_geo<Tl>(L);
+        const int nb = grid(g), nt = 32 * Tl::Warps;
+        const size_t sm = Q == 1 ? sizeof(StSmem<1, Tl>) + 128 : sizeof(StSmem<2, Tl>) + 128;
         ST_DISPATCH_Q12(Q, {
+            // the upwind coupling of every chunk's first slab: one small gather pass (9 mass
+            // entries per row and chunk) before the march
+            const double *cpl = nullptr;
+            if (g.n_chunks > 1 || prev) {
+                const long long n = (long long)L.n_edges * g.n_chunks;
+                k_st_coupling<QQ><<<nblocks(n), kBlock, 0, st>>>(L.n_edges, L.S, g.n_chunks, L.M, x, prev, L.st_cpl);
+                ++g_extra_launches;
+                cpl = L.st_cpl;
+            }
             StMaps maps;
-            stencil_maps<QQ>(L, x, g.n_chunks > 1 || prev, prev ? L.st_halo : nullptr, maps);
+            stencil_maps<QQ, Tl>(L, x, maps);
             auto launch = [&](auto kern) {
                 stencil_smem_attr(kern, (int)sm);
-                kern<<<nb, nt, sm, st>>>(g, *L.st_tab, maps, hp, L.tau, f, r, z, omega_s, kt, partial);
+                kern<<<nb, nt, sm, st>>>(g, *L.st_tab, maps, cpl, L.tau, f, r, z, omega_s, kt, partial);
             };
             if (partial) {
                 if (r) launch(k_st_residual<QQ, true, false, true>);
@@ -1450,7 +1447,7 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
 }
 
 int residual_partials(const DevLevel &L) {
-    if (stencil_applies(L, L.Q)) return grid(stencil_geo(L, L.Q));
+    if (stencil_applies(L, L.Q)) return grid(stencil_geo<StTileRes>(L));
     return (L.use_march && L.Q <= 2) ? grid(march_map(L, true)) : grid(edge_map(L));
 }
 
@@ -1458,12 +1455,13 @@ void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, 
                   const double *r, double *out, double omega_s, double omega) {
     if (stencil_applies(L, Q)) {
         note(V_STENCIL_SWEEP);
-        const StGeo g = stencil_geo(L, Q);
-        const int nb = grid(g), nt = 32 * kStWarps;
-        const size_t sm = Q == 1 ? sizeof(StSmem<1>) + 128 : sizeof(StSmem<2>) + 128;
+        using Tl = StTileSweep;
+        const StGeo g = stencil_geo<Tl>(L);
+        const int nb = grid(g), nt = 32 * Tl::Warps;
+        const size_t sm = Q == 1 ? sizeof(StSmem<1, Tl>) + 128 : sizeof(StSmem<2, Tl>) + 128;
         ST_DISPATCH_Q12(Q, {
             StMaps maps;
-            stencil_maps<QQ>(L, z, false, nullptr, maps);
+            stencil_maps<QQ, Tl>(L, z, maps);
             auto launch = [&](auto kern) {
                 stencil_smem_attr(kern, (int)sm);
                 kern<<<nb, nt, sm, st>>>(g, *L.st_tab, maps, L.tau, r, out, omega_s, omega, kt);
@@ -1575,9 +1573,17 @@ void launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mod
     const int spl = L.S % 2 == 0 ? 2 : 1;
     if (L.S > 32 * spl) note(V_SCAN_MULTI);
     if (carry) note(V_SCAN_CARRY);
+    // compile-time K_n widths of the hex (27) and quad (9) node stencils: the gathers of one slab
+    // chunk are all in flight at once (measured 1.1 TB/s with the runtime-width loop)
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(spl, {
         if (mode == 0) k_node_scan<QQ, SP, 0><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
-        else if (mode == 1) k_node_scan<QQ, SP, 1><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
+        else if (L.Kn.width == 27) {
+            if (mode == 1) k_node_scan<QQ, SP, 1, 27><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
+            else k_node_scan<QQ, SP, 2, 27><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
+        } else if (L.Kn.width == 9) {
+            if (mode == 1) k_node_scan<QQ, SP, 1, 9><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
+            else k_node_scan<QQ, SP, 2, 9><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
+        } else if (mode == 1) k_node_scan<QQ, SP, 1><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
         else k_node_scan<QQ, SP, 2><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
     }));
 }

@@ -16,13 +16,13 @@
 // and s-1, s (Z rows); the rows of level s-1 are then complete and leave through the epilogue:
 // 21 operand reads per node and slab instead of 3 x 33 for three ELL rows, every coefficient load
 // shared by the q+1 time nodes, and the (q+1) x (q+1) time blocks of R1 applied in registers.
-// A CTA is a tile of kStTI x kStTJ pencils of one slab chunk; its z-levels are staged in shared
+// A CTA is a tile of TI x TJ pencils of one slab chunk (StTile); its z-levels are staged in shared
 // memory by TMA (below), halo included, so neighbouring pencils share every operand fetch.
 //
 // Upwind coupling (residual only): time node 0 of slab k needs (M x_q) of slab k-1: inside a warp
-// the mass accumulator of lane k-1 (one shuffle); for the first slab of the chunk the march also
-// accumulates (M x_q) of the slab before it from a staged 2-slab box of the 15 mass-coupled
-// neighbours per level (or from the previous rank's end values `prev`, staged the same way).
+// the mass accumulator of lane k-1 (one shuffle); for the first slab of each 32-slab chunk a small
+// gather pass (k_st_coupling: 9 mass entries per row and chunk, or the previous rank's end values
+// `prev` for chunk 0) runs before the march.
 #pragma once
 
 struct StGeo {
@@ -30,8 +30,18 @@ struct StGeo {
     int S, tiles_i, n_tiles, n_chunks;
 };
 
-constexpr int kStTI = 4, kStTJ = 2;            // pencils per CTA (one warp each)
-constexpr int kStWarps = kStTI * kStTJ;
+// CTA tile: TI x TJ pencils (one warp each) of one 32-slab chunk
+template <int TI_, int TJ_>
+struct StTile {
+    static constexpr int TI = TI_, TJ = TJ_, Warps = TI_ * TJ_;
+    static constexpr int BX = (TI_ + 1) * (TJ_ + 2);            // staged x-edge blocks per level
+    static constexpr int BY = (TI_ + 2) * (TJ_ + 1);
+    static constexpr int BZ = (TI_ + 2) * (TJ_ + 2);
+};
+// 4 x 3 pencils = 12 warps at <= 168 registers (sweep: measured 29.6 vs 34.0 ms per c4 V-cycle
+// for 4 x 2 pencils = 8 warps at 224 registers; 4 x 4 spills)
+using StTileRes = StTile<4, 3>;
+using StTileSweep = StTile<4, 3>;
 constexpr int kStSPW = 32;                     // slabs per warp (lane = slab)
 constexpr int kStInterior = 4;                 // class (1, 1): both transverse coordinates inside
 
@@ -42,22 +52,37 @@ __device__ __forceinline__ double2 st_coef(const StencilTab &tab, int T, int cls
 }
 
 // open accumulators (M x_b, K x_b) per row type, open level and time node b
-// (X, Y rows: levels s-1, s, s+1; Z rows: s-1, s); StPrev: M x_q of the slab before the chunk
+// (X, Y rows: levels s-1, s, s+1; Z rows: s-1, s)
 template <int Q>
 struct StAcc {
     double xm[3][Q], xk[3][Q], ym[3][Q], yk[3][Q], zm[2][Q], zk[2][Q];
-};
-struct StPrev {
-    double x[3], y[3], z[2];
 };
 
 // Push the inputs of z-level s into the open rows.  xin[a][b][q]: x-edge (i-1+a, j-1+b, s), time
 // node q; yin: y-edges (i-1+a, j-1+b, s); zin: z-edges (i-1+a, j-1+b, s).  clsX[d] / clsY[d]:
 // class of the X / Y row at level s-1+d, clsZ: class of the pencil's Z rows.
-template <int Q, bool FAST, bool ZIN>
-__device__ __forceinline__ void st_push(const StencilTab &tab, const double (&xin)[2][3][Q],
-                                        const double (&yin)[3][2][Q], const double (&zin)[3][3][Q],
+#ifndef ST_PHASES
+#define ST_PHASES 1
+#endif
+// compiler-only barrier: keeps the shared-memory reads of the next input group after the FMAs of
+// this one, so that only one group of operands is live at a time (register budget -> warps/SM)
+__device__ __forceinline__ void st_phase() {
+    if (ST_PHASES) asm volatile("" ::: "memory");
+}
+
+// xs / ys / zs: the warp's x-, y-, z-edge input blocks of the staged level, element (a, b, q) at
+// [(b * row + a) * Blk + q * 32] with row = the tile-box i extent of the edge type
+template <int Q, class Tl, bool FAST, bool ZIN>
+__device__ __forceinline__ void st_push(const StencilTab &tab, const double *xs, const double *ys, const double *zs,
                                         const int (&clsX)[3], const int (&clsY)[3], int clsZ, StAcc<Q> &A) {
+    constexpr int Blk = Q * kStSPW;
+    double xin[2][3][Q], yin[3][2][Q], zin[3][3][Q];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+            for (int q = 0; q < Q; ++q) xin[a][b][q] = xs[(b * (Tl::TI + 1) + a) * Blk + q * kStSPW];
     // loop order: input outermost, then the open levels d and time nodes q innermost, so that
     // consecutive FMAs go to independent accumulators (latency of the fp64 pipe)
     // ---- x-edge inputs xin[a][b] = x-edge (i-1+a, j-1+b)
@@ -90,6 +115,13 @@ __device__ __forceinline__ void st_push(const StencilTab &tab, const double (&xi
             }
         }
     // ---- y-edge inputs yin[a][b] = y-edge (i-1+a, j-1+b)
+    st_phase();
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int q = 0; q < Q; ++q) yin[a][b][q] = ys[(b * (Tl::TI + 2) + a) * Blk + q * kStSPW];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -120,6 +152,13 @@ __device__ __forceinline__ void st_push(const StencilTab &tab, const double (&xi
         }
     // ---- z-edge inputs zin[a][b] = z-edge (i-1+a, j-1+b) from level s to s+1
     if (ZIN) {
+        st_phase();
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b)
+#pragma unroll
+                for (int q = 0; q < Q; ++q) zin[a][b][q] = zs[(b * (Tl::TI + 2) + a) * Blk + q * kStSPW];
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
@@ -148,30 +187,6 @@ __device__ __forceinline__ void st_push(const StencilTab &tab, const double (&xi
     }
 }
 
-// the mass-coupled part of st_push for the slab before the chunk (time node q only)
-template <bool FAST, bool ZIN>
-__device__ __forceinline__ void st_push_prev(const StencilTab &tab, const double (&xp)[3], const double (&yp)[3],
-                                             const double (&zp)[3][3], const int (&clsX)[3], const int (&clsY)[3],
-                                             int clsZ, StPrev &B) {
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        const int o2 = 1 - d;
-#pragma unroll
-        for (int b = 0; b < 3; ++b)
-            B.x[d] = fma(st_coef<FAST>(tab, 0, clsX[d], st_slot(0, 0, 0, b - 1, o2)).x, xp[b], B.x[d]);
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-            B.y[d] = fma(st_coef<FAST>(tab, 1, clsY[d], st_slot(1, 1, a - 1, 0, o2)).x, yp[a], B.y[d]);
-    }
-    if (ZIN) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b)
-                B.z[1] = fma(st_coef<FAST>(tab, 2, clsZ, st_slot(2, 2, a - 1, b - 1, 0)).x, zp[a][b], B.z[1]);
-    }
-}
-
 // ------------------------------------------------------------- TMA staging
 // Each z-level's inputs of the whole CTA tile are staged in shared memory by three 5-D TMA tile
 // loads (cp.async.bulk.tensor, one elected thread, completion on an mbarrier), kStNB levels ahead
@@ -181,33 +196,25 @@ __device__ __forceinline__ void st_push_prev(const StencilTab &tab, const double
 // zero-filled by the TMA unit, so the march needs no index clamping: every missing neighbour reads
 // 0 and has a zero coefficient anyway.  The box lands as [j][i][time node][slab]: a warp reads its
 // 21 x (q+1) inputs with conflict-free 8-byte LDS (lane = slab) at compile-time offsets.
-constexpr int kStNB = 3;                                    // staged z-levels in flight
-constexpr int kStBX = (kStTI + 1) * (kStTJ + 2);            // x-edge blocks per level
-constexpr int kStBY = (kStTI + 2) * (kStTJ + 1);
-constexpr int kStBZ = (kStTI + 2) * (kStTJ + 2);
-// the (slab k0-2, k0-1) pair of time node q per block; every TMA destination starts 128-byte aligned
-constexpr int kStPrevPart = 48;                             // doubles: >= 24 blocks x 2, multiple of 16
-constexpr int kStPrevLevel = 3 * kStPrevPart;
-static_assert(kStBX * 2 <= kStPrevPart && kStBY * 2 <= kStPrevPart && kStBZ * 2 <= kStPrevPart, "prev part");
-
-template <int Q>
+#ifndef ST_NB
+#define ST_NB 3
+#endif
+constexpr int kStNB = ST_NB;                                // staged z-levels in flight
+template <int Q, class Tl>
 struct StCfg {
     static constexpr int Blk = Q * kStSPW;                              // doubles per edge block
-    static constexpr int Level = (kStBX + kStBY + kStBZ) * Blk;         // doubles per staged level
-    static_assert((kStBX * Blk * 8) % 128 == 0 && (kStBY * Blk * 8) % 128 == 0 && (Level * 8) % 128 == 0,
+    static constexpr int Level = (Tl::BX + Tl::BY + Tl::BZ) * Blk;      // doubles per staged level
+    static_assert((Tl::BX * Blk * 8) % 128 == 0 && (Tl::BY * Blk * 8) % 128 == 0 && (Level * 8) % 128 == 0,
                   "TMA destinations must stay 128-byte aligned");
 };
 
 struct StMaps {
     CUtensorMap x, y, z;            // the input vector's x-, y-, z-edge blocks
-    CUtensorMap px, py, pz;         // the same vector, box = slab pair (k0-2, k0-1) of time node q
-    CUtensorMap hx, hy, hz;         // the previous rank's end values staged as slab 1 of a 2-slab vector
 };
 
-template <int Q>
+template <int Q, class Tl>
 struct alignas(128) StSmem {
-    double buf[kStNB][StCfg<Q>::Level];
-    double prev[kStNB][kStPrevLevel];
+    double buf[kStNB][StCfg<Q, Tl>::Level];
     unsigned long long full[kStNB];
 };
 
@@ -243,31 +250,20 @@ __device__ __forceinline__ void st_tma_5d(void *dst, const CUtensorMap *map, int
 }
 
 // issue the staging of z-level s into buffer s % kStNB (one thread)
-template <int Q, bool PREVM>
-__device__ __forceinline__ void st_stage(const StGeo &g, const StMaps &maps, StSmem<Q> &sm, int s, int i0, int j0,
+template <int Q, class Tl>
+__device__ __forceinline__ void st_stage(const StGeo &g, const StMaps &maps, StSmem<Q, Tl> &sm, int s, int i0, int j0,
                                          int k0) {
-    using C = StCfg<Q>;
+    using C = StCfg<Q, Tl>;
     const int nb = s % kStNB;
     const bool zin = s < g.nz;
-    constexpr unsigned bx = kStBX * C::Blk * 8, by = kStBY * C::Blk * 8, bz = kStBZ * C::Blk * 8;
-    constexpr unsigned px = kStBX * 16, py = kStBY * 16, pz = kStBZ * 16;
-    unsigned bytes = bx + by + (zin ? bz : 0);
-    if (PREVM) bytes += px + py + (zin ? pz : 0);
+    constexpr unsigned bx = Tl::BX * C::Blk * 8, by = Tl::BY * C::Blk * 8, bz = Tl::BZ * C::Blk * 8;
+    const unsigned bytes = bx + by + (zin ? bz : 0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     st_mbar_expect(&sm.full[nb], bytes);
     double *b = sm.buf[nb];
     st_tma_5d(b, &maps.x, k0, 0, i0 - 1, j0 - 1, s, &sm.full[nb]);
-    st_tma_5d(b + kStBX * C::Blk, &maps.y, k0, 0, i0 - 1, j0 - 1, s, &sm.full[nb]);
-    if (zin) st_tma_5d(b + (kStBX + kStBY) * C::Blk, &maps.z, k0, 0, i0 - 1, j0 - 1, s, &sm.full[nb]);
-    if (PREVM) {
-        // (M x_q) of the slab before the chunk: slab k0 - 1 of x, or the previous rank's end values
-        double *p = sm.prev[nb];
-        const bool h = k0 == 0;
-        const int c0 = h ? 0 : k0 - 2;
-        st_tma_5d(p, h ? &maps.hx : &maps.px, c0, Q - 1, i0 - 1, j0 - 1, s, &sm.full[nb]);
-        st_tma_5d(p + kStPrevPart, h ? &maps.hy : &maps.py, c0, Q - 1, i0 - 1, j0 - 1, s, &sm.full[nb]);
-        if (zin) st_tma_5d(p + 2 * kStPrevPart, h ? &maps.hz : &maps.pz, c0, Q - 1, i0 - 1, j0 - 1, s, &sm.full[nb]);
-    }
+    st_tma_5d(b + Tl::BX * C::Blk, &maps.y, k0, 0, i0 - 1, j0 - 1, s, &sm.full[nb]);
+    if (zin) st_tma_5d(b + (Tl::BX + Tl::BY) * C::Blk, &maps.z, k0, 0, i0 - 1, j0 - 1, s, &sm.full[nb]);
 }
 
 // Lane constants: slab k, tau_k, and per row type T the Jacobi block D = Ct dM + tau_k Mt dK of the
@@ -351,16 +347,16 @@ __device__ __forceinline__ void st_time(const KT &kt, const StLane<Q> &L, const 
 
 // The march of one CTA tile (one pencil per warp) over all z-levels.  Op supplies
 // pre(T, row, own) (own-row values of the rows completing at this step; own = the staged block of
-// the row at its level) and emit<FAST>(T, row, cls, m[Q], k[Q], mprev); every warp reaches every
+// the row at its level) and emit<FAST>(T, row, cls, m[Q], k[Q]); every warp reaches every
 // barrier (also warps whose pencil lies outside the mesh).
-template <int Q, bool PREVM, class Op>
-__device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, const StMaps &maps, StSmem<Q> &sm,
+template <int Q, class Tl, class Op>
+__device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, const StMaps &maps, StSmem<Q, Tl> &sm,
                                          int tile, int chunk, Op &op) {
-    using C = StCfg<Q>;
+    using C = StCfg<Q, Tl>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ti = tile % g.tiles_i, tj = tile / g.tiles_i;
-    const int i0 = ti * kStTI, j0 = tj * kStTJ;
-    const int wi = warp % kStTI, wj = warp / kStTI;
+    const int i0 = ti * Tl::TI, j0 = tj * Tl::TJ;
+    const int wi = warp % Tl::TI, wj = warp / Tl::TI;
     const int i = i0 + wi, j = j0 + wj;
     const bool ok = i <= g.nx && j <= g.ny;
     const int k0 = chunk * kStSPW;
@@ -371,27 +367,21 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
     }
     __syncthreads();
     if (threadIdx.x == 0)
-        for (int s = 0; s < kStNB && s <= g.nz; ++s) st_stage<Q, PREVM>(g, maps, sm, s, i0, j0, k0);
+        for (int s = 0; s < kStNB && s <= g.nz; ++s) st_stage<Q, Tl>(g, maps, sm, s, i0, j0, k0);
     StAcc<Q> A;
-    StPrev B;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
+    for (int d = 0; d < 3; ++d)
 #pragma unroll
         for (int q = 0; q < Q; ++q) A.xm[d][q] = A.xk[d][q] = A.ym[d][q] = A.yk[d][q] = 0.0;
-        B.x[d] = B.y[d] = 0.0;
-    }
 #pragma unroll
     for (int q = 0; q < Q; ++q) A.zm[0][q] = A.zk[0][q] = A.zm[1][q] = A.zk[1][q] = 0.0;
-    B.z[0] = B.z[1] = 0.0;
     const int ci = st_cls(i, g.nx), cj = st_cls(j, g.ny);
     const bool inner_pencil = ci == 1 && cj == 1;
     const int clsZ = 3 * ci + cj;
     // the warp's block offsets inside a staged level (doubles)
-    const int ox = (wj * (kStTI + 1) + wi) * C::Blk + lane;
-    const int oy = kStBX * C::Blk + (wj * (kStTI + 2) + wi) * C::Blk + lane;
-    const int oz = (kStBX + kStBY) * C::Blk + (wj * (kStTI + 2) + wi) * C::Blk + lane;
-    const int pox = (wj * (kStTI + 1) + wi) * 2 + 1, poy = kStPrevPart + (wj * (kStTI + 2) + wi) * 2 + 1;
-    const int poz = 2 * kStPrevPart + (wj * (kStTI + 2) + wi) * 2 + 1;
+    const int ox = (wj * (Tl::TI + 1) + wi) * C::Blk + lane;
+    const int oy = Tl::BX * C::Blk + (wj * (Tl::TI + 2) + wi) * C::Blk + lane;
+    const int oz = (Tl::BX + Tl::BY) * C::Blk + (wj * (Tl::TI + 2) + wi) * C::Blk + lane;
     for (int s = 0; s <= g.nz + 1; ++s) {
         const int l = s - 1;                   // level of the rows that complete at this step
         const unsigned rX = (unsigned)(i + g.nx * (j + (g.ny + 1) * l));
@@ -399,51 +389,18 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
         const unsigned rZ = (unsigned)(g.Ex + g.Ey + i + (g.nx + 1) * (j + (g.ny + 1) * l));
         const bool eX = ok && s >= 1 && i < g.nx, eY = ok && s >= 1 && j < g.ny, eZ = ok && s >= 1 && l < g.nz;
         const double *lb = sm.buf[(s + kStNB - 1) % kStNB];         // level s-1 (own values)
-        if (eX) op.pre(0, rX, lb + ox + C::Blk * ((kStTI + 1) + 1));
-        if (eY) op.pre(1, rY, lb + oy + C::Blk * ((kStTI + 2) + 1));
-        if (eZ) op.pre(2, rZ, lb + oz + C::Blk * ((kStTI + 2) + 1));
+        if (eX) op.pre(0, rX, lb + ox + C::Blk * ((Tl::TI + 1) + 1));
+        if (eY) op.pre(1, rY, lb + oy + C::Blk * ((Tl::TI + 2) + 1));
+        if (eZ) op.pre(2, rZ, lb + oz + C::Blk * ((Tl::TI + 2) + 1));
         const bool fast = inner_pencil && s >= 2 && s <= g.nz - 2;
         if (s <= g.nz) {
             const int nb = s % kStNB;
             st_mbar_wait(&sm.full[nb], (unsigned)((s / kStNB) & 1));
             const double *bb = sm.buf[nb];
-            double xin[2][3][Q], yin[3][2][Q], zin[3][3][Q];
-#pragma unroll
-            for (int a = 0; a < 2; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) xin[a][b][q] = bb[ox + (b * (kStTI + 1) + a) * C::Blk + q * kStSPW];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 2; ++b)
-#pragma unroll
-                    for (int q = 0; q < Q; ++q) yin[a][b][q] = bb[oy + (b * (kStTI + 2) + a) * C::Blk + q * kStSPW];
             const bool zin_ok = s < g.nz;
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-#pragma unroll
-                for (int b = 0; b < 3; ++b)
-#pragma unroll
-                    for (int q = 0; q < Q; ++q)
-                        zin[a][b][q] = zin_ok ? bb[oz + (b * (kStTI + 2) + a) * C::Blk + q * kStSPW] : 0.0;
-            double xp[3], yp[3], zp[3][3];
-            if (PREVM) {
-                const double *pb = sm.prev[nb];
-#pragma unroll
-                for (int b = 0; b < 3; ++b) xp[b] = pb[pox + (b * (kStTI + 1) + 1) * 2];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) yp[a] = pb[poy + ((kStTI + 2) + a) * 2];
-#pragma unroll
-                for (int a = 0; a < 3; ++a)
-#pragma unroll
-                    for (int b = 0; b < 3; ++b) zp[a][b] = zin_ok ? pb[poz + (b * (kStTI + 2) + a) * 2] : 0.0;
-            }
             if (fast) {
                 const int dummy[3] = {0, 0, 0};
-                st_push<Q, true, true>(tab, xin, yin, zin, dummy, dummy, clsZ, A);
-                if (PREVM) st_push_prev<true, true>(tab, xp, yp, zp, dummy, dummy, clsZ, B);
+                st_push<Q, Tl, true, true>(tab, bb + ox, bb + oy, bb + oz, dummy, dummy, clsZ, A);
             } else {
                 int clsX[3], clsY[3];
 #pragma unroll
@@ -453,24 +410,22 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
                     clsY[d] = 3 * ci + cl;
                 }
                 if (zin_ok) {
-                    st_push<Q, false, true>(tab, xin, yin, zin, clsX, clsY, clsZ, A);
-                    if (PREVM) st_push_prev<false, true>(tab, xp, yp, zp, clsX, clsY, clsZ, B);
+                    st_push<Q, Tl, false, true>(tab, bb + ox, bb + oy, bb + oz, clsX, clsY, clsZ, A);
                 } else {
-                    st_push<Q, false, false>(tab, xin, yin, zin, clsX, clsY, clsZ, A);
-                    if (PREVM) st_push_prev<false, false>(tab, xp, yp, zp, clsX, clsY, clsZ, B);
+                    st_push<Q, Tl, false, false>(tab, bb + ox, bb + oy, bb + oz, clsX, clsY, clsZ, A);
                 }
             }
         }
         if (s >= 1) {
             const int cl = st_cls(l, g.nz);
             if (fast) {
-                if (eX) op.template emit<true>(0, rX, kStInterior, A.xm[0], A.xk[0], B.x[0]);
-                if (eY) op.template emit<true>(1, rY, kStInterior, A.ym[0], A.yk[0], B.y[0]);
-                if (eZ) op.template emit<true>(2, rZ, kStInterior, A.zm[0], A.zk[0], B.z[0]);
+                if (eX) op.template emit<true>(0, rX, kStInterior, A.xm[0], A.xk[0]);
+                if (eY) op.template emit<true>(1, rY, kStInterior, A.ym[0], A.yk[0]);
+                if (eZ) op.template emit<true>(2, rZ, kStInterior, A.zm[0], A.zk[0]);
             } else {
-                if (eX) op.template emit<false>(0, rX, 3 * cj + cl, A.xm[0], A.xk[0], B.x[0]);
-                if (eY) op.template emit<false>(1, rY, 3 * ci + cl, A.ym[0], A.yk[0], B.y[0]);
-                if (eZ) op.template emit<false>(2, rZ, clsZ, A.zm[0], A.zk[0], B.z[0]);
+                if (eX) op.template emit<false>(0, rX, 3 * cj + cl, A.xm[0], A.xk[0]);
+                if (eY) op.template emit<false>(1, rY, 3 * ci + cl, A.ym[0], A.yk[0]);
+                if (eZ) op.template emit<false>(2, rZ, clsZ, A.zm[0], A.zk[0]);
             }
         }
 #pragma unroll
@@ -482,16 +437,11 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
             A.zm[0][q] = A.zm[1][q]; A.zm[1][q] = 0.0;
             A.zk[0][q] = A.zk[1][q]; A.zk[1][q] = 0.0;
         }
-        if (PREVM) {
-            B.x[0] = B.x[1]; B.x[1] = B.x[2]; B.x[2] = 0.0;
-            B.y[0] = B.y[1]; B.y[1] = B.y[2]; B.y[2] = 0.0;
-            B.z[0] = B.z[1]; B.z[1] = 0.0;
-        }
         // every warp is done with level s-1 (own values) and level s: refill the buffer of
         // level s-1 with level s-1+kStNB
         __syncthreads();
         if (threadIdx.x == 0 && s >= 1 && s - 1 + kStNB <= g.nz)
-            st_stage<Q, PREVM>(g, maps, sm, s - 1 + kStNB, i0, j0, k0);
+            st_stage<Q, Tl>(g, maps, sm, s - 1 + kStNB, i0, j0, k0);
     }
 }
 
@@ -516,21 +466,22 @@ struct StResOp {
     size_t bstride;
     double omega_s;
     bool first;                     // lane of the chunk's first slab
+    const double *cpl;              // (M x_q) of the slab before this chunk, per row (k_st_coupling), or null
     double nrm;
-    double fv[3][Q];
+    double fv[3][Q], cv[3];
     __device__ __forceinline__ void pre(int T, unsigned row, const double *) {
         const char *p = fb + (size_t)row * rowbytes;
 #pragma unroll
         for (int b = 0; b < Q; ++b) fv[T][b] = __ldg(reinterpret_cast<const double *>(p + b * bstride));
+        cv[T] = first && cpl ? __ldg(cpl + row) : 0.0;     // null: chunk 0, zero initial state
     }
     template <bool FAST>
-    __device__ __forceinline__ void emit(int T, unsigned row, int cls, const double (&m)[Q], const double (&k)[Q],
-                                         double mprev) {
+    __device__ __forceinline__ void emit(int T, unsigned row, int cls, const double (&m)[Q], const double (&k)[Q]) {
         double ax[Q], rr[Q];
         st_time<Q>(kt, L, m, k, ax);
         // upwind coupling on time node 0: (M x_q)(k-1), lane k-1's mass accumulator of node q
         const double up = __shfl_up_sync(0xffffffffu, m[Q - 1], 1);
-        const double mp = first ? mprev : up;
+        const double mp = first ? cv[T] : up;
 #pragma unroll
         for (int b = 0; b < Q; ++b) rr[b] = fv[T][b] - ax[b] + (b == 0 ? mp : 0.0);
         const size_t off = (size_t)row * rowbytes;
@@ -554,13 +505,15 @@ struct StResOp {
     }
 };
 
-template <int Q, bool R_OUT, bool Z_OUT, bool NORM>
-__global__ void __launch_bounds__(32 * kStWarps, 1)
-k_st_residual(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constant__ StMaps maps, int has_prev,
-              const double *__restrict__ tau, const double *__restrict__ f, double *__restrict__ r,
-              double *__restrict__ z, double omega_s, KT kt, double *__restrict__ partial) {
+// cpl: the coupling of each chunk's first slab from k_st_coupling ([chunk][row]), or null when there
+// is none (a single chunk and the zero initial state)
+template <int Q, bool R_OUT, bool Z_OUT, bool NORM, class Tl = StTileRes>
+__global__ void __launch_bounds__(32 * Tl::Warps, 1)
+k_st_residual(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constant__ StMaps maps,
+              const double *__restrict__ cpl, const double *__restrict__ tau, const double *__restrict__ f,
+              double *__restrict__ r, double *__restrict__ z, double omega_s, KT kt, double *__restrict__ partial) {
     extern __shared__ __align__(128) unsigned char st_dyn[];
-    StSmem<Q> &sm = *reinterpret_cast<StSmem<Q> *>(st_dyn + ((128u - (st_smem_addr(st_dyn) & 127u)) & 127u));
+    StSmem<Q, Tl> &sm = *reinterpret_cast<StSmem<Q, Tl> *>(st_dyn + ((128u - (st_smem_addr(st_dyn) & 127u)) & 127u));
     __shared__ StBlockTab<Q> bt;
     const int chunk = blockIdx.x / g.n_tiles, tile = blockIdx.x - chunk * g.n_tiles;
     StLane<Q> L;
@@ -569,12 +522,15 @@ k_st_residual(StGeo g, const __grid_constant__ StencilTab tab, const __grid_cons
     const unsigned rowbytes = (unsigned)(8u * Q * g.S);
     const size_t lane_off = (size_t)L.k * 8;
     StResOp<Q, R_OUT, Z_OUT, NORM> op{tab, kt, L, bt, reinterpret_cast<const char *>(f) + lane_off,
-                                      reinterpret_cast<char *>(r) + lane_off, reinterpret_cast<char *>(z) + lane_off,
-                                      rowbytes, (size_t)g.S * 8, omega_s, (threadIdx.x & 31) == 0, 0.0, {}};
-    if (chunk > 0 || has_prev) st_march<Q, true>(g, tab, maps, sm, tile, chunk, op);
-    else st_march<Q, false>(g, tab, maps, sm, tile, chunk, op);
+                                           reinterpret_cast<char *>(r) + lane_off,
+                                           reinterpret_cast<char *>(z) + lane_off, rowbytes, (size_t)g.S * 8, omega_s,
+                                           (threadIdx.x & 31) == 0,
+                                           cpl ? cpl + (size_t)chunk * (g.Ex + g.Ey + (g.nx + 1) * (g.ny + 1) * g.nz)
+                                               : nullptr,
+                                           0.0, {}, {}};
+    st_march<Q, Tl>(g, tab, maps, sm, tile, chunk, op);
     if (NORM) {
-        __shared__ double sh[kStWarps];
+        __shared__ double sh[Tl::Warps];
         const double s = block_reduce_sum(op.nrm, sh);
         if (threadIdx.x == 0) partial[blockIdx.x] = s;
     }
@@ -604,8 +560,7 @@ struct StSweepOp {
         }
     }
     template <bool FAST>
-    __device__ __forceinline__ void emit(int T, unsigned row, int cls, const double (&m)[Q], const double (&k)[Q],
-                                         double) {
+    __device__ __forceinline__ void emit(int T, unsigned row, int cls, const double (&m)[Q], const double (&k)[Q]) {
         double D[Q * Q], Di[Q * Q], az[Q], d[Q];
         st_row_block<Q, FAST>(tab, kt, L, bt, T, cls, D, Di);
         st_time<Q>(kt, L, m, k, az);
@@ -636,13 +591,13 @@ struct StSweepOp {
     }
 };
 
-template <int Q, bool LAST, bool RECON>
-__global__ void __launch_bounds__(32 * kStWarps, 1)
+template <int Q, bool LAST, bool RECON, class Tl = StTileSweep>
+__global__ void __launch_bounds__(32 * Tl::Warps, 1)
 k_st_sweep(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constant__ StMaps maps,
            const double *__restrict__ tau, const double *__restrict__ r, double *out, double omega_s, double omega,
            KT kt) {
     extern __shared__ __align__(128) unsigned char st_dyn[];
-    StSmem<Q> &sm = *reinterpret_cast<StSmem<Q> *>(st_dyn + ((128u - (st_smem_addr(st_dyn) & 127u)) & 127u));
+    StSmem<Q, Tl> &sm = *reinterpret_cast<StSmem<Q, Tl> *>(st_dyn + ((128u - (st_smem_addr(st_dyn) & 127u)) & 127u));
     __shared__ StBlockTab<Q> bt;
     const int chunk = blockIdx.x / g.n_tiles, tile = blockIdx.x - chunk * g.n_tiles;
     StLane<Q> L;
@@ -653,5 +608,35 @@ k_st_sweep(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constan
     StSweepOp<Q, LAST, RECON> op{tab, kt, L, bt, reinterpret_cast<const char *>(r) + lane_off,
                                  reinterpret_cast<char *>(out) + lane_off, rowbytes, (size_t)g.S * 8, omega_s, omega,
                                  {}, {}, {}};
-    st_march<Q, false>(g, tab, maps, sm, tile, chunk, op);
+    st_march<Q, Tl>(g, tab, maps, sm, tile, chunk, op);
+}
+
+// (M x_q) of the slab before every 32-slab chunk (chunk c >= 1: slab 32c - 1) and, with prev, the
+// previous rank's end values (chunk 0): the upwind coupling of each chunk's first slab
+// (N_t = e_0 e_q^T), out[c * n_edges + row]; one thread per (row, chunk)
+template <int Q>
+__global__ void __launch_bounds__(256) k_st_coupling(int n_edges, int S, int n_chunks, DevELL M,
+                                                      const double *__restrict__ x, const double *__restrict__ prev,
+                                                      double *__restrict__ out) {
+    const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (id >= (long long)n_edges * n_chunks) return;
+    const int c = (int)(id / n_edges), row = (int)(id - (long long)c * n_edges);
+    double acc = 0.0;
+    const Ent *e = M.e + (size_t)row * M.width;
+    if (c == 0) {
+        if (prev)
+            for (int s = 0; s < M.width; ++s) {
+                double v; int col;
+                ld_ent(e + s, v, col);
+                acc = fma(v, __ldg(prev + col), acc);
+            }
+    } else {
+        const size_t off = (size_t)(Q - 1) * S + (size_t)c * kStSPW - 1;
+        for (int s = 0; s < M.width; ++s) {
+            double v; int col;
+            ld_ent(e + s, v, col);
+            acc = fma(v, __ldg(x + (size_t)col * Q * S + off), acc);
+        }
+    }
+    out[id] = acc;
 }

@@ -1,6 +1,3 @@
-python scripts/srchash.py > gpurun_out/r2_l_srchash.txt
-python bench.py > gpurun_out/r2_l_bench.json 2> gpurun_out/r2_l_bench.err
-python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2_l_plain.log 2>&1 &&
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_l_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2_l_ncu1.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:"k_st_" -c 2 -o gpurun_out/r2_l_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2_l_ncu2.log 2>&1
-du -sh gpurun_out
+timeout 300 python scripts/variant_check.py paper_1911_09548_b200/libst.so 3 > gpurun_out/r2_n_variant.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_stencil.py tests/test_gpu_bench_paths.py tests/test_gpu_distributed.py -q -x -p no:cacheprovider > gpurun_out/r2_n_tests.log 2>&1; echo rc=$? >> gpurun_out/r2_n_tests.log
+cat gpurun_out/r2_n_variant.log; tail -3 gpurun_out/r2_n_tests.log
