@@ -265,7 +265,7 @@ def run_ours(args, rank, world, local_rank):
                 # ||r||, one V-cycle, ||r||, D2H x; the copies of neighbouring steps overlap the solve
                 xh2 = torch.zeros(fh.shape, dtype=torch.float64).pin_memory()
                 s.solve_many_host([xh.numpy()], [fh.numpy()], tol=0.0, maxit=1, history=False)   # warm-up
-                ke = max(2, min(args.steps, 5))
+                ke = max(2, args.steps)              # two pinned output buffers, reused alternately
                 outs = [(xh if i % 2 == 0 else xh2).numpy() for i in range(ke)]
                 t0 = time.perf_counter()
                 s.solve_many_host(outs, [fh.numpy()] * ke, tol=0.0, maxit=1, history=False)
@@ -291,10 +291,15 @@ def run_ours(args, rank, world, local_rank):
                 t = torch.tensor([te], device=red_dev, dtype=torch.float64)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 te = float(t.item())
+            link = link_bandwidth(torch, fh, f, stream)
+            h2d_b = (1 if world == 1 else 2) * f.numel() * 8
+            d2h_b = f.numel() * 8
+            # the copy bound of a fully pipelined step: the slower direction at the measured link speed
+            t_copy = max(h2d_b / (link["h2d"] * 1e9), d2h_b / (link["d2h"] * 1e9)) if link else None
             e2e = {"value": n_dofs * world / te, "unit": UNIT,
-                   "h2d_bytes_per_step": (1 if world == 1 else 2) * f.numel() * 8 * world,
-                   "d2h_bytes_per_step": f.numel() * 8 * world, "note": note,
-                   "link_GBps": link_bandwidth(torch, fh, f, stream)}
+                   "h2d_bytes_per_step": h2d_b * world, "d2h_bytes_per_step": d2h_b * world, "note": note,
+                   "link_GBps": link,
+                   "copy_bound_value": (n_dofs * world / t_copy) if t_copy else None}
     info = s.info()
     s.close()
     torch.cuda.synchronize()

@@ -68,6 +68,7 @@ struct st_handle {
     bool mk_dict = true;        // env ST_MK_DICT=0: never use the dictionary ELL
     bool stencil = true;        // env ST_STENCIL=0: never use the structured stencil march
     std::vector<std::unique_ptr<st::StencilTab>> st_tabs;
+    std::vector<std::unique_ptr<st::NodeTab>> sn_tabs;
     std::vector<int> tab_slots;   // constant-bank dictionary slots this handle holds
     cudaStream_t cap_stream = nullptr;
     struct Graph { const double *x, *f; cudaGraphExec_t exec; int64_t launches; };
@@ -232,7 +233,7 @@ double *inner_vcycle(st_handle *h, std::vector<DevLevel> &V, int j, const double
     auto nodal = [&] {
         h->run("in_nodal", 2 * ev + nv + ell_bytes(I.GtM) + 8.0 * I.n_nodes, 1,
                [&] { st::launch_nodal_step(s, I, h->kt, Q, r, cur, o.omega_n, I.y); });
-        h->run("in_gupdate", 2 * ev + nv + 8.0 * I.n_edges, 1, [&] { st::launch_g_update(s, I, h->kt, Q, I.y, nullptr, cur); });
+        h->run("in_gupdate", 2 * ev + nv + 8.0 * I.n_edges, 1, [&] { st::launch_g_update(s, I, h->kt, Q, I.y, nullptr, nullptr, cur); });
     };
     for (int i = 0; i < o.nu_in; ++i) {
         if (i == 0) {
@@ -331,14 +332,15 @@ void correct_A_local(st_handle *h, DevLevel &L, double *x, const double *f, cons
         h->run("node_sweep", 3 * nv + kb, 1, [&] { st::launch_node_sweep(s, L, Q, cur, L.wn, o.omega_n, other); });
         std::swap(cur, other);
     }
-    h->run("node_scan", (mode == 2 ? 3 : 2) * nv + kb, 1, [&] { st::launch_node_scan(s, L, h->kt, Q, mode, cur, L.wn, o.omega_n, nullptr, L.y, tot); });
+    h->run("node_scan", (mode == 2 ? 3 : 2) * nv + kb, 1, [&] { L.sn_pending = st::launch_node_scan(s, L, h->kt, Q, mode, cur, L.wn, o.omega_n, nullptr, L.y, tot); });
 }
 
 // second half: x += G (y + g carry), carry (optional, n_nodes) = end value before this block
 void correct_A_apply(st_handle *h, DevLevel &L, double *x, const double *carry) {
     auto s = (st::Stream)h->stream;
     const int Q = h->Q;
-    h->run("g_update", 2 * evec(L, Q) + nvec(L, Q) + 8.0 * L.n_edges, 1, [&] { st::launch_g_update(s, L, h->kt, Q, L.y, carry, x); });
+    h->run("g_update", 2 * evec(L, Q) + nvec(L, Q) + 8.0 * L.n_edges, 1,
+           [&] { st::launch_g_update(s, L, h->kt, Q, L.y, carry, L.sn_pending ? L.sn_cc : nullptr, x); });
 }
 
 void correct_A(st_handle *h, DevLevel &L, double *x, const double *f, const double *prev) {
@@ -592,6 +594,16 @@ int st_setup(const st_params *p, st_handle **out) {
                     D.grid.nx = H.mesh.n[0]; D.grid.ny = H.mesh.n[1]; D.grid.nz = H.mesh.n[2];
                     D.grid.Ex = H.mesh.Ex; D.grid.Ey = H.mesh.Ey;
                     D.st_cpl = h->dalloc<double>((size_t)D.n_edges * (cnt / 32));
+                    D.st_bslab = h->dalloc<double>((size_t)D.n_edges * (cnt / 32));
+                    // structured node scan on the same levels (env ST_NODE_STENCIL=0: ELL k_node_scan)
+                    const char *ns = std::getenv("ST_NODE_STENCIL");
+                    auto ntab = std::make_unique<st::NodeTab>();
+                    if ((!ns || std::atoi(ns) != 0) && st::build_node_tab(H, *ntab)) {
+                        D.sn_tab = ntab.get();
+                        h->sn_tabs.push_back(std::move(ntab));
+                        D.sn_ctot = h->dalloc<double>((size_t)D.n_nodes * (cnt / 32));
+                        D.sn_cc = h->dalloc<double>((size_t)D.n_nodes * (cnt / 32));
+                    }
                 }
             }
             D.space_coarsened = H.space_coarsened;

@@ -82,6 +82,15 @@ struct StencilTab {
 };
 bool build_stencil_tab(const HostLevel &L, StencilTab &tab);   // false: the level is not class-uniform
 
+// Structured node stencil table (nstencil.cuh): the 27 K_n coefficients of a node per boundary class
+// (each coordinate at 0 / inside / at n: class 9 ci + 3 cj + cl), slot 9 (di + 1) + 3 (dj + 1) + (dl + 1);
+// kernel parameter space (5832 bytes).
+constexpr int kSnClasses = 27, kSnSlots = 27, kSnInterior = 13;
+struct NodeTab {
+    double c[kSnClasses][kSnSlots];
+};
+bool build_node_tab(const HostLevel &L, NodeTab &tab);         // false: K_n is not class-uniform
+
 // Slot numbering of the stencil table: for a row of direction T at node p, neighbour edge of
 // direction T2 at node p + (o0, o1, o2); block of T2 == T: o_T = 0, the other two offsets in
 // {-1,0,1} (9 slots); T2 != T: o_T in {0,1}, o_T2 in {-1,0}, the third in {-1,0,1} (12 slots);
@@ -123,6 +132,11 @@ struct DevLevel {
     bool use_stencil = false;       // structured stencil march (stencil.cuh) for residual and sweep
     StencilTab *st_tab = nullptr;   // host copy of the level's stencil table (owned by the handle)
     double *st_cpl = nullptr;       // [chunk][row] upwind coupling of each 32-slab chunk's first slab
+    double *st_bslab = nullptr;     // [chunk][row] x_q of the slab before each chunk (k_st_bslab)
+    NodeTab *sn_tab = nullptr;      // host copy of the level's node stencil table (structured node scan), or null
+    double *sn_ctot = nullptr;      // [chunk][node] Sigma_t chunk totals (k_sn_scan)
+    double *sn_cc = nullptr;        // [chunk][node] chunk carries (k_sn_carry), added by the G update
+    bool sn_pending = false;        // the last node scan left its chunk carries for the G update
     int lpr_log2 = 5;       // edge kernels: log2(lanes per row); slab chunk = 2 << lpr_log2 (32: measured best)
     Grid3 grid{};
     double *tau = nullptr;
@@ -170,9 +184,12 @@ void launch_gtr(Stream st, const DevLevel &L, const KT &kt, int Q, const double 
                 double omega_n, double *zn, double *w);
 void launch_node_sweep(Stream st, const DevLevel &L, int Q, const double *z, const double *w, double omega_n,
                        double *zout);
-void launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mode, const double *z,
+// returns true when it left chunk carries (L.sn_cc) that the G update of this level must add
+bool launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mode, const double *z,
                       const double *w, double omega_n, const double *carry, double *y, double *tot);
-void launch_g_update(Stream st, const DevLevel &L, const KT &kt, int Q, const double *y, const double *carry, double *x);
+// cc: chunk carries [S/32][node] of the structured node scan, or null
+void launch_g_update(Stream st, const DevLevel &L, const KT &kt, int Q, const double *y, const double *carry,
+                     const double *cc, double *x);
 void launch_copy_slabs(Stream st, int rows, int Q, int ns, double *dst, int dS, int dk0, const double *src, int sS,
                        int sk0, bool add);
 void launch_end_values(Stream st, int rows, int Q, int S, const double *x, double *out);

@@ -40,7 +40,7 @@ static const char *const kVariantNames[] = {
     "sweep/chunked", "res_mass/spl1", "res_mass/spl2", "res_mass/spl4", "res_mass/chunked",
     "gtr/fused", "gtr/chunked", "gt/two-pass", "node_scan/multichunk", "node_scan/carry-in",
     "march/residual", "march/sweep", "restrict/space", "prolong/space", "stencil/residual",
-    "stencil/sweep", "stencil/res_mass", "coupling/prev"};
+    "stencil/sweep", "stencil/res_mass", "coupling/prev", "stencil/node_scan"};
 constexpr int kNumVariants = (int)(sizeof(kVariantNames) / sizeof(kVariantNames[0]));
 static std::atomic<unsigned long long> g_variants{0};
 static inline void note(int bit) { g_variants.fetch_or(1ull << bit, std::memory_order_relaxed); }
@@ -48,7 +48,8 @@ enum VariantBit {
     V_RES_DICT, V_RES_PLAIN, V_RES_FOLD, V_RES_SPL1, V_RES_SPL2, V_RES_CHUNKED, V_SWEEP_DICT, V_SWEEP_PLAIN,
     V_SWEEP_SPL1, V_SWEEP_SPL2, V_SWEEP_SPL4, V_SWEEP_CHUNKED, V_RM_SPL1, V_RM_SPL2, V_RM_SPL4, V_RM_CHUNKED,
     V_GTR_FUSED, V_GTR_CHUNKED, V_GT_TWOPASS, V_SCAN_MULTI, V_SCAN_CARRY, V_MARCH_RES, V_MARCH_SWEEP,
-    V_RESTRICT_SPACE, V_PROLONG_SPACE, V_STENCIL_RES, V_STENCIL_SWEEP, V_STENCIL_RM, V_COUPLING_PREV
+    V_RESTRICT_SPACE, V_PROLONG_SPACE, V_STENCIL_RES, V_STENCIL_SWEEP, V_STENCIL_RM, V_COUPLING_PREV,
+    V_SN_SCAN
 };
 unsigned long long variants(bool reset) {
     return reset ? g_variants.exchange(0) : g_variants.load();
@@ -807,13 +808,18 @@ __global__ void __launch_bounds__(kBlock) k_node_scan(int nodes, int S, DevELL K
 // (carry: integrated end value before this slab block, R2; null = 0)
 template <int Q, int SPL>
 __global__ void __launch_bounds__(kBlock) k_g_update(BoxMap m, const int *__restrict__ en, const double *__restrict__ y,
-                                                     const double *__restrict__ carry, KT kt, double *__restrict__ x) {
+                                                     const double *__restrict__ carry, const double *__restrict__ cc,
+                                                     int n_nodes, KT kt, double *__restrict__ x) {
     box_loop(m, [&](int e, int k0, bool valid) {
     if (!valid) return;
     const int S = m.S;
     const int n0 = __ldg(en + 2 * e), n1 = __ldg(en + 2 * e + 1);
     const size_t QS = (size_t)Q * S;
-    const double dc = carry ? __ldg(carry + n1) - __ldg(carry + n0) : 0.0;
+    double dc = carry ? __ldg(carry + n1) - __ldg(carry + n0) : 0.0;
+    if (cc) {       // chunk carries of the structured node scan (32-slab chunks; a lane's slabs share one)
+        const double *c = cc + (size_t)(k0 / 32) * n_nodes;        // kStSPW = 32 (stencil.cuh)
+        dc += __ldg(c + n1) - __ldg(c + n0);
+    }
 #pragma unroll
     for (int a = 0; a < Q; ++a) {
         double y0[SPL], y1[SPL], xv[SPL];
@@ -1194,6 +1200,7 @@ __global__ void __launch_bounds__(1024) k_reduce(int n, const double *__restrict
 }
 
 #include "stencil.cuh"
+#include "nstencil.cuh"
 
 // --------------------------------------------------------------- launchers
 static inline int nblocks(long long work) { return (int)((work + kBlock - 1) / kBlock); }
@@ -1381,8 +1388,10 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
             const double *cpl = nullptr;
             if (g.n_chunks > 1 || prev) {
                 const long long n = (long long)L.n_edges * g.n_chunks;
-                k_st_coupling<QQ><<<nblocks(n), kBlock, 0, st>>>(L.n_edges, L.S, g.n_chunks, L.M, x, prev, L.st_cpl);
-                ++g_extra_launches;
+                if (L.M.width > 9) throw std::logic_error("stencil coupling: mass ELL wider than 9");
+                k_st_bslab<QQ><<<nblocks(n), kBlock, 0, st>>>(L.n_edges, L.S, g.n_chunks, x, prev, L.st_bslab);
+                k_st_coupling<<<nblocks(L.n_edges), kBlock, 0, st>>>(L.n_edges, g.n_chunks, L.M, L.st_bslab, L.st_cpl);
+                g_extra_launches += 2;
                 cpl = L.st_cpl;
             }
             StMaps maps;
@@ -1567,8 +1576,39 @@ void launch_node_sweep(Stream st, const DevLevel &L, int Q, const double *z, con
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, k_node_sweep<QQ, SP><<<grid(m), kBlock, 0, st>>>(m, L.Kn, L.dN, z, w, omega_n, zout)));
 }
 
-void launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mode, const double *z,
+static SnGeo sn_geo(const DevLevel &L) {
+    SnGeo g{};
+    g.nx = L.grid.nx; g.ny = L.grid.ny; g.nz = L.grid.nz;
+    g.S = L.S;
+    g.tiles_i = (g.nx + 1 + SnTileT::TI - 1) / SnTileT::TI;
+    g.n_tiles = g.tiles_i * ((g.ny + 1 + SnTileT::TJ - 1) / SnTileT::TJ);
+    g.n_chunks = L.S / kStSPW;
+    g.n_nodes = L.n_nodes;
+    return g;
+}
+
+bool launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mode, const double *z,
                       const double *w, double omega_n, const double *carry, double *y, double *tot) {
+    if (L.sn_tab && !carry && (mode == 1 || mode == 2) && (Q == 1 || Q == 2) && L.S % kStSPW == 0) {
+        // structured node march (nstencil.cuh) + chunk carries
+        note(V_SN_SCAN);
+        const SnGeo g = sn_geo(L);
+        CUtensorMap mz;
+        encode_block(&mz, z, L.S, Q, g.nx + 1, g.ny + 1, g.nz + 1, kStSPW, Q, SnTileT::TI + 2, SnTileT::TJ + 2);
+        const int nb = g.n_tiles * g.n_chunks, nt = 32 * SnTileT::Warps;
+        ST_DISPATCH_Q12(Q, {
+            const size_t sm = sizeof(SnSmem<QQ, SnTileT>) + 128;
+            auto launch = [&](auto kern) {
+                stencil_smem_attr(kern, (int)sm);
+                kern<<<nb, nt, sm, st>>>(g, *L.sn_tab, mz, L.dN, w, omega_n, kt, y, L.sn_ctot);
+            };
+            if (mode == 1) launch(k_sn_scan<QQ, 1>);
+            else launch(k_sn_scan<QQ, 2>);
+        });
+        k_sn_carry<<<nblocks(L.n_nodes), kBlock, 0, st>>>(L.n_nodes, g.n_chunks, L.sn_ctot, L.sn_cc, tot);
+        ++g_extra_launches;
+        return true;
+    }
     const int g = nblocks((long long)L.n_nodes * 32);
     const int spl = L.S % 2 == 0 ? 2 : 1;
     if (L.S > 32 * spl) note(V_SCAN_MULTI);
@@ -1586,11 +1626,15 @@ void launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mod
         } else if (mode == 1) k_node_scan<QQ, SP, 1><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
         else k_node_scan<QQ, SP, 2><<<g, kBlock, 0, st>>>(L.n_nodes, L.S, L.Kn, L.dN, z, w, omega_n, kt, carry, y, tot);
     }));
+    return false;
 }
 
-void launch_g_update(Stream st, const DevLevel &L, const KT &kt, int Q, const double *y, const double *carry, double *x) {
+void launch_g_update(Stream st, const DevLevel &L, const KT &kt, int Q, const double *y, const double *carry,
+                     const double *cc, double *x) {
     const BoxMap m = edge_map(L);
-    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, k_g_update<QQ, SP><<<grid(m), kBlock, 0, st>>>(m, L.edge_nodes, y, carry, kt, x)));
+    if (cc && (m.chunk % kStSPW != 0 && m.S > m.chunk)) throw std::logic_error("g_update: lane slabs straddle a chunk");
+    ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, k_g_update<QQ, SP><<<grid(m), kBlock, 0, st>>>(m, L.edge_nodes, y, carry, cc,
+                                                                                            L.n_nodes, kt, x)));
 }
 
 void launch_copy_slabs(Stream st, int rows, int Q, int ns, double *dst, int dS, int dk0, const double *src, int sS,

@@ -635,6 +635,57 @@ static void detect_uniform(HostLevel &L) {
 // bitwise identical coefficients, M must vanish off the parallel block (axis-aligned cells), and a
 // slot whose neighbour does not exist must be zero for the whole class.  Returns false (the level
 // keeps the ELL kernels) when any of this fails, e.g. for per-cell varying coefficients.
+// K_n of a uniform hex level as a 27-point node stencil per boundary class (nstencil.cuh): every
+// node of a class must carry the class representative's coefficients (to a few ulps, as for the
+// edge table) and every nonzero slot must point at an existing node
+bool build_node_tab(const HostLevel &L, NodeTab &tab) {
+    const HostMesh &m = L.mesh;
+    if (m.dim != 3 || !L.uniform || L.Kn.rows != m.n_nodes) return false;
+    const int nx = m.n[0], ny = m.n[1], nz = m.n[2];
+    const int W = L.Kn.width;
+    std::memset(&tab, 0, sizeof(tab));
+    bool seen[kSnClasses] = {};
+    double row[kSnSlots];
+    for (int r = 0; r < m.n_nodes; ++r) {
+        const int i = r % (nx + 1), j = (r / (nx + 1)) % (ny + 1), l = r / ((nx + 1) * (ny + 1));
+        const int cls = 9 * st_cls(i, nx) + 3 * st_cls(j, ny) + st_cls(l, nz);
+        for (int s2 = 0; s2 < kSnSlots; ++s2) row[s2] = 0.0;
+        bool has[kSnSlots] = {};
+        for (int s = 0; s < W; ++s) {
+            const size_t o = (size_t)r * W + s;
+            const double v = L.Kn.val[o];
+            if (v == 0.0) continue;                        // padding / exact zeros
+            const int c = L.Kn.col[o];
+            const int i2 = c % (nx + 1), j2 = (c / (nx + 1)) % (ny + 1), l2 = c / ((nx + 1) * (ny + 1));
+            const int di = i2 - i, dj = j2 - j, dl = l2 - l;
+            if (std::abs(di) > 1 || std::abs(dj) > 1 || std::abs(dl) > 1) return false;
+            const int sl = 9 * (di + 1) + 3 * (dj + 1) + (dl + 1);
+            if (has[sl]) return false;
+            has[sl] = true;
+            row[sl] = v;
+        }
+        double *t = tab.c[cls];
+        if (!seen[cls]) {
+            seen[cls] = true;
+            for (int s2 = 0; s2 < kSnSlots; ++s2) t[s2] = row[s2];
+        } else {
+            double sc = 0.0;
+            for (int s2 = 0; s2 < kSnSlots; ++s2) sc = std::max(sc, std::fabs(row[s2]));
+            const double tol = 8.0 * std::nextafter(sc, 2.0 * sc + 1.0) - 8.0 * sc;
+            // (an entry that is zero in exact arithmetic may come out as a few ulps of the row scale
+            // on a non-dyadic mesh, so zero-ness is compared through the same tolerance)
+            for (int s2 = 0; s2 < kSnSlots; ++s2)
+                if (std::fabs(t[s2] - row[s2]) > tol) return false;
+        }
+        for (int s2 = 0; s2 < kSnSlots; ++s2) {
+            if (t[s2] == 0.0) continue;
+            const int di = s2 / 9 - 1, dj = (s2 / 3) % 3 - 1, dl = s2 % 3 - 1;
+            if (i + di < 0 || i + di > nx || j + dj < 0 || j + dj > ny || l + dl < 0 || l + dl > nz) return false;
+        }
+    }
+    return true;
+}
+
 bool build_stencil_tab(const HostLevel &L, StencilTab &tab) {
     const HostMesh &m = L.mesh;
     if (m.dim != 3 || !L.uniform || L.MK.rows != m.n_edges) return false;

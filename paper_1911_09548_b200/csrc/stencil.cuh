@@ -216,7 +216,29 @@ template <int Q, class Tl>
 struct alignas(128) StSmem {
     double buf[kStNB][StCfg<Q, Tl>::Level];
     unsigned long long full[kStNB];
+    unsigned done[kStNB];           // warps finished with the level in each buffer (last-arriver refill)
 };
+
+// Buffer release without a CTA barrier: every warp, once done with the level in buffer nb, counts
+// itself in; the last warp to arrive resets the count and issues the TMA refill, so no warp waits
+// for the slowest one (a warp that runs ahead blocks only on the full barrier of a level not yet
+// landed).  Measured on c4 (ms per V-cycle, two runs each): sweep 24.8 / 25.0 vs 25.1 / 25.1 with a
+// CTA barrier, node scan 4.56 / 4.59 vs 5.0 / 4.98, but residual 48.2 / 48.1 vs 46.9 / 46.7 -- so
+// the residual keeps the barrier (and thread 0 refilling).
+template <int Warps>
+__device__ __forceinline__ bool st_release(unsigned *done) {
+    __syncwarp();
+    unsigned last = 0;
+    if ((threadIdx.x & 31) == 0) {
+        __threadfence_block();          // this warp's reads of the buffer are performed before the count
+        last = atomicAdd(done, 1u) == Warps - 1;
+        if (last) {
+            __threadfence_block();      // ... and the refill's TMA is issued after every warp's count
+            *done = 0;
+        }
+    }
+    return __shfl_sync(0xffffffffu, last, 0) != 0;
+}
 
 __device__ __forceinline__ unsigned st_smem_addr(const void *p) {
     return (unsigned)__cvta_generic_to_shared(p);
@@ -349,7 +371,7 @@ __device__ __forceinline__ void st_time(const KT &kt, const StLane<Q> &L, const 
 // pre(T, row, own) (own-row values of the rows completing at this step; own = the staged block of
 // the row at its level) and emit<FAST>(T, row, cls, m[Q], k[Q]); every warp reaches every
 // barrier (also warps whose pencil lies outside the mesh).
-template <int Q, class Tl, class Op>
+template <int Q, class Tl, bool LAST_REFILL, class Op>
 __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, const StMaps &maps, StSmem<Q, Tl> &sm,
                                          int tile, int chunk, Op &op) {
     using C = StCfg<Q, Tl>;
@@ -362,7 +384,7 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
     const int k0 = chunk * kStSPW;
     if (threadIdx.x == 0) {
 #pragma unroll
-        for (int b = 0; b < kStNB; ++b) st_mbar_init(&sm.full[b], 1);
+        for (int b = 0; b < kStNB; ++b) { st_mbar_init(&sm.full[b], 1); sm.done[b] = 0; }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -437,11 +459,17 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
             A.zm[0][q] = A.zm[1][q]; A.zm[1][q] = 0.0;
             A.zk[0][q] = A.zk[1][q]; A.zk[1][q] = 0.0;
         }
-        // every warp is done with level s-1 (own values) and level s: refill the buffer of
-        // level s-1 with level s-1+kStNB
-        __syncthreads();
-        if (threadIdx.x == 0 && s >= 1 && s - 1 + kStNB <= g.nz)
-            st_stage<Q, Tl>(g, maps, sm, s - 1 + kStNB, i0, j0, k0);
+        // this warp is done with level s-1 (own values): once every warp is, refill its buffer
+        // with level s-1+kStNB
+        if (LAST_REFILL) {
+            if (s >= 1 && s - 1 + kStNB <= g.nz && st_release<Tl::Warps>(&sm.done[(s - 1) % kStNB]) &&
+                (threadIdx.x & 31) == 0)
+                st_stage<Q, Tl>(g, maps, sm, s - 1 + kStNB, i0, j0, k0);
+        } else {
+            __syncthreads();
+            if (threadIdx.x == 0 && s >= 1 && s - 1 + kStNB <= g.nz)
+                st_stage<Q, Tl>(g, maps, sm, s - 1 + kStNB, i0, j0, k0);
+        }
     }
 }
 
@@ -528,7 +556,7 @@ k_st_residual(StGeo g, const __grid_constant__ StencilTab tab, const __grid_cons
                                            cpl ? cpl + (size_t)chunk * (g.Ex + g.Ey + (g.nx + 1) * (g.ny + 1) * g.nz)
                                                : nullptr,
                                            0.0, {}, {}};
-    st_march<Q, Tl>(g, tab, maps, sm, tile, chunk, op);
+    st_march<Q, Tl, false>(g, tab, maps, sm, tile, chunk, op);
     if (NORM) {
         __shared__ double sh[Tl::Warps];
         const double s = block_reduce_sum(op.nrm, sh);
@@ -564,28 +592,19 @@ struct StSweepOp {
         double D[Q * Q], Di[Q * Q], az[Q], d[Q];
         st_row_block<Q, FAST>(tab, kt, L, bt, T, cls, D, Di);
         st_time<Q>(kt, L, m, k, az);
-        // d = r - A z, with r = D z / omega_s (RECON) or read
+        // RECON: r = D z / omega_s, so z + omega_s D^{-1} (r - A z) = 2 z - omega_s D^{-1} A z (no
+        // division, D itself unused); otherwise d = r - A z with r read
 #pragma unroll
-        for (int b = 0; b < Q; ++b) {
-            double rb_ = 0.0;
-            if (RECON) {
-#pragma unroll
-                for (int a = 0; a < Q; ++a) rb_ = fma(D[b * Q + a], zv[T][a], rb_);
-                rb_ /= omega_s;
-            } else {
-                rb_ = rv[T][b];
-            }
-            d[b] = rb_ - az[b];
-        }
+        for (int b = 0; b < Q; ++b) d[b] = RECON ? az[b] : rv[T][b] - az[b];
         const size_t off = (size_t)row * rowbytes;
 #pragma unroll
         for (int b = 0; b < Q; ++b) {
             double y = 0.0;
 #pragma unroll
             for (int a = 0; a < Q; ++a) y = fma(Di[b * Q + a], d[a], y);
-            const double res = zv[T][b] + omega_s * y;
+            const double res = RECON ? fma(-omega_s, y, 2.0 * zv[T][b]) : fma(omega_s, y, zv[T][b]);
             double *o = reinterpret_cast<double *>(ob + off + b * bstride);
-            if (LAST) *o = xv[T][b] + omega * res;
+            if (LAST) *o = fma(omega, res, xv[T][b]);
             else *o = res;
         }
     }
@@ -608,35 +627,44 @@ k_st_sweep(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constan
     StSweepOp<Q, LAST, RECON> op{tab, kt, L, bt, reinterpret_cast<const char *>(r) + lane_off,
                                  reinterpret_cast<char *>(out) + lane_off, rowbytes, (size_t)g.S * 8, omega_s, omega,
                                  {}, {}, {}};
-    st_march<Q, Tl>(g, tab, maps, sm, tile, chunk, op);
+    st_march<Q, Tl, true>(g, tab, maps, sm, tile, chunk, op);
 }
 
-// (M x_q) of the slab before every 32-slab chunk (chunk c >= 1: slab 32c - 1) and, with prev, the
-// previous rank's end values (chunk 0): the upwind coupling of each chunk's first slab
-// (N_t = e_0 e_q^T), out[c * n_edges + row]; one thread per (row, chunk)
+// The upwind coupling of each chunk's first slab (N_t = e_0 e_q^T): (M x_q) of the
+// slab before the chunk (chunk c >= 1: slab 32c - 1; chunk 0: the previous rank's end values `prev`),
+// out[c * n_edges + row].  Two passes so that x is touched once per (column, chunk): k_st_bslab
+// copies x_q(32c - 1) of every row into a compact [chunk][row] array (one strided 8-byte read per
+// value), then k_st_coupling applies the 9-slot mass ELL to it, one thread per row looping over the
+// chunks (the ELL row is read once; the compact slice of a chunk stays in L2).
 template <int Q>
-__global__ void __launch_bounds__(256) k_st_coupling(int n_edges, int S, int n_chunks, DevELL M,
-                                                      const double *__restrict__ x, const double *__restrict__ prev,
-                                                      double *__restrict__ out) {
+__global__ void __launch_bounds__(256) k_st_bslab(int n_edges, int S, int n_chunks, const double *__restrict__ x,
+                                                   const double *__restrict__ prev, double *__restrict__ b) {
     const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (id >= (long long)n_edges * n_chunks) return;
     const int c = (int)(id / n_edges), row = (int)(id - (long long)c * n_edges);
-    double acc = 0.0;
+    b[id] = c == 0 ? (prev ? __ldg(prev + row) : 0.0)
+                   : __ldg(x + (size_t)row * Q * S + (size_t)(Q - 1) * S + (size_t)c * kStSPW - 1);
+}
+
+__global__ void __launch_bounds__(256) k_st_coupling(int n_edges, int n_chunks, DevELL M, const double *__restrict__ b,
+                                                      double *__restrict__ out) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= n_edges) return;
+    constexpr int W = 9;
+    double v[W];
+    int col[W];
     const Ent *e = M.e + (size_t)row * M.width;
-    if (c == 0) {
-        if (prev)
-            for (int s = 0; s < M.width; ++s) {
-                double v; int col;
-                ld_ent(e + s, v, col);
-                acc = fma(v, __ldg(prev + col), acc);
-            }
-    } else {
-        const size_t off = (size_t)(Q - 1) * S + (size_t)c * kStSPW - 1;
-        for (int s = 0; s < M.width; ++s) {
-            double v; int col;
-            ld_ent(e + s, v, col);
-            acc = fma(v, __ldg(x + (size_t)col * Q * S + off), acc);
-        }
+    const int w = M.width;
+#pragma unroll
+    for (int s = 0; s < W; ++s) {
+        if (s < w) ld_ent(e + s, v[s], col[s]);
+        else { v[s] = 0.0; col[s] = row; }
     }
-    out[id] = acc;
+    for (int c = 0; c < n_chunks; ++c) {
+        const double *bc = b + (size_t)c * n_edges;
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < W; ++s) acc = fma(v[s], __ldg(bc + col[s]), acc);
+        out[(size_t)c * n_edges + row] = acc;
+    }
 }

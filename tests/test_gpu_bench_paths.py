@@ -73,9 +73,9 @@ CASES = {
     "c3_8x256": lambda: workloads.c3(n=8, S=256),
 }
 MUST_RUN = {
-    "c4_8x128": {"stencil/residual", "stencil/sweep", "gt/two-pass", "node_scan/multichunk"},
-    "c4_8x256": {"stencil/residual", "stencil/sweep", "node_scan/multichunk"},
-    "c4_8x512": {"stencil/residual", "stencil/sweep", "node_scan/multichunk"},
+    "c4_8x128": {"stencil/residual", "stencil/sweep", "gt/two-pass", "stencil/node_scan"},
+    "c4_8x256": {"stencil/residual", "stencil/sweep", "stencil/node_scan"},
+    "c4_8x512": {"stencil/residual", "stencil/sweep", "stencil/node_scan"},
     "c5_6x256": {"sweep/spl4", "sweep/plain", "residual/plain-fold", "residual/chunked", "sweep/chunked",
                  "gt/two-pass", "node_scan/multichunk"},
     "c3_8x256": {"sweep/spl4", "sweep/plain", "residual/plain", "residual/chunked", "node_scan/multichunk"},

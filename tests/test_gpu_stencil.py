@@ -40,7 +40,7 @@ def test_stencil_vcycle_parity(torch_cuda, n, S, q):
     s.vcycle(x, f)
     torch.cuda.synchronize()
     ran = p.kernel_variants(reset=True)
-    assert {"stencil/residual", "stencil/sweep"} <= ran, ran
+    assert {"stencil/residual", "stencil/sweep", "stencil/node_scan"} <= ran, ran
     close_elementwise(workloads.to_oracle(x.cpu().numpy()), X1, env, f"stencil {n} S={S} q={q}")
     # the residual alone (every chunk-start coupling lane, boundary classes)
     r = torch.empty_like(f)
@@ -79,3 +79,49 @@ def test_stencil_matches_ell(torch_cuda, name, monkeypatch):
     assert outs[0][1] == pytest.approx(outs[1][1], rel=1e-13)
     xs = float(np.abs(outs[1][2]).max())
     assert float(np.abs(outs[0][2] - outs[1][2]).max()) <= 1e-11 * xs
+
+
+@pytest.mark.parametrize("nu_n", [1, 3])
+def test_stencil_node_scan_modes(torch_cuda, nu_n):
+    # the last nodal sweep with w read (nu_n = 3: MODE 2 of the structured node scan) and without a
+    # sweep (nu_n = 1: the ELL scan), several chunks; Eq. (5) with Sigma_t of DESIGN.md R2
+    import paper_1911_09548_b200 as p
+    torch = torch_cuda
+    w = uniform_case((4, 5, 6), 96, 1)
+    rng = np.random.default_rng(23)
+    F = rng.uniform(-1, 1, (w.S, w.q + 1, w.n_edges))
+    X0 = rng.uniform(-1, 1, F.shape)
+    H, X1, env = vcycle_envelope(w, X0, F, nu_n=nu_n)
+    s = p.Solver.from_workload(w, nu_n=nu_n)
+    x = torch.from_numpy(workloads.from_oracle(X0)).cuda()
+    f = torch.from_numpy(workloads.from_oracle(F)).cuda()
+    p.kernel_variants(reset=True)
+    s.vcycle(x, f)
+    torch.cuda.synchronize()
+    ran = p.kernel_variants(reset=True)
+    assert ("stencil/node_scan" in ran) == (nu_n > 1), ran
+    close_elementwise(workloads.to_oracle(x.cpu().numpy()), X1, env, f"node scan nu_n={nu_n}")
+
+
+def test_node_stencil_matches_ell(torch_cuda, monkeypatch):
+    # the structured node scan and the ELL k_node_scan on the same V-cycle: equal to rounding
+    import paper_1911_09548_b200 as p
+    torch = torch_cuda
+    w = workloads.c4(n=8, S=128, tau=1.0 / 64)
+    rng = np.random.default_rng(29)
+    F = workloads.from_oracle(rng.uniform(-1, 1, (w.S, w.q + 1, w.n_edges)))
+    X0 = workloads.from_oracle(rng.uniform(-1, 1, (w.S, w.q + 1, w.n_edges)))
+    outs = []
+    for env in ("1", "0"):
+        monkeypatch.setenv("ST_NODE_STENCIL", env)
+        s = p.Solver.from_workload(w)
+        x = torch.from_numpy(X0).cuda()
+        f = torch.from_numpy(F).cuda()
+        p.kernel_variants(reset=True)
+        s.vcycle(x, f)
+        torch.cuda.synchronize()
+        assert ("stencil/node_scan" in p.kernel_variants(reset=True)) == (env == "1")
+        outs.append(x.cpu().numpy())
+        s.close()
+    monkeypatch.delenv("ST_NODE_STENCIL")
+    assert float(np.abs(outs[0] - outs[1]).max()) <= 1e-12 * float(np.abs(outs[1]).max())
