@@ -122,7 +122,7 @@ def ncu_traffic(family):
     if cap.get("source_hash") != srchash():
         return None, f"capture {os.path.basename(p)} is of other kernel sources ({cap.get('source_hash')} vs {srchash()})"
     tags = {"residual": ("k_st_residual<", "k_residual<"), "sweep_update": ("k_st_sweep<", "k_sweep<"),
-            "node_scan": ("k_node_scan<",), "gt": ("k_gt<",)}.get(family, ())
+            "node_scan": ("k_sn_scan<", "k_node_scan<"), "gt": ("k_gt<",)}.get(family, ())
 
     def gb(v):
         val, unit = v.split()[:2]

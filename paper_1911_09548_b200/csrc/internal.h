@@ -88,6 +88,7 @@ bool build_stencil_tab(const HostLevel &L, StencilTab &tab);   // false: the lev
 constexpr int kSnClasses = 27, kSnSlots = 27, kSnInterior = 13;
 struct NodeTab {
     double c[kSnClasses][kSnSlots];
+    double dinv[kSnClasses];        // 1 / the class's diagonal (the Jacobi divisor d_n)
 };
 bool build_node_tab(const HostLevel &L, NodeTab &tab);         // false: K_n is not class-uniform
 

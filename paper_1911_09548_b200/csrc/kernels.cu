@@ -1073,13 +1073,32 @@ __global__ void __launch_bounds__(kBlock) k_jacobi_point(Map m, const double *__
     for (int a = 0; a < Q; ++a) z[base + a * S] = omega * y[a];
 }
 
+// The (2Q x Q) time matrices of the CTA's coarse slabs (one slab chunk, <= 32 slabs) staged in shared
+// memory as Ps[entry][slab]: every lane reads its own slab's entries conflict-free, instead of 2Q^2
+// loads per thread that each span 32 x 64 bytes (the L1 wavefronts of those loads bounded k_prolong)
+template <int Q>
+__device__ __forceinline__ void stage_pt(const Map &m, const double *__restrict__ Pt, double (*Ps)[32]) {
+    constexpr int N = 2 * Q * Q;
+    const int K0 = (blockIdx.x / m.n_rowblocks) * m.chunk;
+    for (int t = threadIdx.x; t < N * m.chunk; t += blockDim.x) {
+        const int kk = t / N, idx = t - kk * N;
+        if (K0 + kk < m.S) Ps[idx][kk] = __ldg(Pt + (size_t)(K0 + kk) * N + idx);
+    }
+    __syncthreads();
+}
+
 template <int Q, bool SPACE>
 __global__ void __launch_bounds__(kBlock) k_restrict(Map m, DevELL Rg, const double *__restrict__ r,
                                                      const double *__restrict__ Pt, double *__restrict__ fc) {
+    __shared__ double Ps[2 * Q * Q][32];
+    stage_pt<Q>(m, Pt, Ps);
     int rc, K;
     if (!map_thread(m, rc, K)) return;
     const int Sc = m.S, S = 2 * Sc;
-    const double *P = Pt + (size_t)K * 2 * Q * Q;
+    const int kk = K - (blockIdx.x / m.n_rowblocks) * m.chunk;
+    double P[2 * Q * Q];
+#pragma unroll
+    for (int i = 0; i < 2 * Q * Q; ++i) P[i] = Ps[i][kk];
     double acc[Q];
 #pragma unroll
     for (int a = 0; a < Q; ++a) acc[a] = 0.0;
@@ -1099,7 +1118,7 @@ __global__ void __launch_bounds__(kBlock) k_restrict(Map m, DevELL Rg, const dou
         for (int a = 0; a < Q; ++a) {
             double t = 0.0;
 #pragma unroll
-            for (int jb = 0; jb < 2 * Q; ++jb) t += __ldg(P + jb * Q + a) * fv[jb];
+            for (int jb = 0; jb < 2 * Q; ++jb) t += P[jb * Q + a] * fv[jb];
             acc[a] = fma(wgt, t, acc[a]);
         }
     }
@@ -1113,8 +1132,11 @@ __global__ void __launch_bounds__(kBlock) k_restrict(Map m, DevELL Rg, const dou
 template <int Q, bool SPACE>
 __global__ void __launch_bounds__(kBlock) k_prolong(Map m, DevELL Pg, const double *__restrict__ xc,
                                                     const double *__restrict__ Pt, double *__restrict__ x) {
+    __shared__ double Ps[2 * Q * Q][32];
+    stage_pt<Q>(m, Pt, Ps);
     int rf, K;
     if (!map_thread(m, rf, K)) return;
+    const int kk = K - (blockIdx.x / m.n_rowblocks) * m.chunk;
     const int Sc = m.S, S = 2 * Sc;
     double v[Q];
 #pragma unroll
@@ -1128,15 +1150,14 @@ __global__ void __launch_bounds__(kBlock) k_prolong(Map m, DevELL Pg, const doub
 #pragma unroll
         for (int a = 0; a < Q; ++a) v[a] = fma(wgt, __ldg(xr + a * Sc), v[a]);
     }
-    const double *P = Pt + (size_t)K * 2 * Q * Q;
     const size_t base = (size_t)rf * Q * S + 2 * K;
 #pragma unroll
     for (int b = 0; b < Q; ++b) {
         double t0 = 0.0, t1 = 0.0;
 #pragma unroll
         for (int a = 0; a < Q; ++a) {
-            t0 += __ldg(P + b * Q + a) * v[a];
-            t1 += __ldg(P + (Q + b) * Q + a) * v[a];
+            t0 += Ps[b * Q + a][kk] * v[a];
+            t1 += Ps[(Q + b) * Q + a][kk] * v[a];
         }
         double2 *px = reinterpret_cast<double2 *>(x + base + b * S);
         double2 xv = *px;
@@ -1600,7 +1621,7 @@ bool launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mod
             const size_t sm = sizeof(SnSmem<QQ, SnTileT>) + 128;
             auto launch = [&](auto kern) {
                 stencil_smem_attr(kern, (int)sm);
-                kern<<<nb, nt, sm, st>>>(g, *L.sn_tab, mz, L.dN, w, omega_n, kt, y, L.sn_ctot);
+                kern<<<nb, nt, sm, st>>>(g, *L.sn_tab, mz, w, omega_n, kt, y, L.sn_ctot);
             };
             if (mode == 1) launch(k_sn_scan<QQ, 1>);
             else launch(k_sn_scan<QQ, 2>);

@@ -8,7 +8,7 @@
 // every coefficient follows from the node numbering of include/st.h.  A warp marches a pencil of
 // nodes (i, j) along z for one 32-slab chunk (lane = slab); the CTA tile's z-levels of the input
 // z_n, halo included, are staged in shared memory by 5-D TMA loads (zero fill outside the mesh)
-// kStNB levels ahead, exactly as the edge march does.  Per node and slab:
+// kSnNB levels ahead (the edge march's scheme; deeper, as a node level is little work).  Per node and slab:
 //   z2 = z + omega_n (w - K_n z) / d_n      (MODE 1: w = d_n z / omega_n, i.e. z2 = 2 z - omega_n K_n z / d_n)
 //   u  = Ct^{-1} z2,  s = u_q,  y = u + g e_{k-1},  e the prefix sum of s over the slabs
 // The prefix sum runs over the 32 slabs of the chunk (warp scan); each chunk's total goes to
@@ -38,11 +38,19 @@ struct SnCfg {
     static_assert((Level * 8) % 128 == 0, "TMA destinations must stay 128-byte aligned");
 };
 
+// staged z-levels in flight: a node level is ~1/10 of an edge level's work, so three levels ahead
+// (the edge march's depth) leave the TMA latency exposed (10 % of the issued instructions were the
+// mbarrier spin in the ncu capture); 6 x 18 KB still fits two CTAs per SM
+#ifndef SN_NB
+#define SN_NB 6
+#endif
+constexpr int kSnNB = SN_NB;
+
 template <int Q, class Tl>
 struct alignas(128) SnSmem {
-    double buf[kStNB][SnCfg<Q, Tl>::Level];
-    unsigned long long full[kStNB];
-    unsigned done[kStNB];
+    double buf[kSnNB][SnCfg<Q, Tl>::Level];
+    unsigned long long full[kSnNB];
+    unsigned done[kSnNB];
 };
 
 template <bool FAST>
@@ -78,7 +86,7 @@ template <int Q, class Tl>
 __device__ __forceinline__ void sn_stage(const SnGeo &g, const CUtensorMap *map, SnSmem<Q, Tl> &sm, int s, int i0, int j0,
                                          int k0) {
     constexpr unsigned bytes = SnCfg<Q, Tl>::Level * 8;
-    const int nb = s % kStNB;
+    const int nb = s % kSnNB;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     st_mbar_expect(&sm.full[nb], bytes);
     st_tma_5d(sm.buf[nb], map, k0, 0, i0 - 1, j0 - 1, s, &sm.full[nb]);
@@ -87,7 +95,7 @@ __device__ __forceinline__ void sn_stage(const SnGeo &g, const CUtensorMap *map,
 template <int Q, int MODE, class Tl = SnTileT>
 __global__ void __launch_bounds__(32 * Tl::Warps, 2)
 k_sn_scan(SnGeo g, const __grid_constant__ NodeTab tab, const __grid_constant__ CUtensorMap mapz,
-          const double *__restrict__ dN, const double *__restrict__ w, double omega_n, KT kt, double *__restrict__ y,
+          const double *__restrict__ w, double omega_n, KT kt, double *__restrict__ y,
           double *__restrict__ ctot) {
     using C = SnCfg<Q, Tl>;
     extern __shared__ __align__(128) unsigned char sn_dyn[];
@@ -101,12 +109,12 @@ k_sn_scan(SnGeo g, const __grid_constant__ NodeTab tab, const __grid_constant__ 
     const int k0 = chunk * kStSPW;
     if (threadIdx.x == 0) {
 #pragma unroll
-        for (int b = 0; b < kStNB; ++b) { st_mbar_init(&sm.full[b], 1); sm.done[b] = 0; }
+        for (int b = 0; b < kSnNB; ++b) { st_mbar_init(&sm.full[b], 1); sm.done[b] = 0; }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (threadIdx.x == 0)
-        for (int s = 0; s < kStNB && s <= g.nz; ++s) sn_stage<Q, Tl>(g, &mapz, sm, s, i0, j0, k0);
+        for (int s = 0; s < kSnNB && s <= g.nz; ++s) sn_stage<Q, Tl>(g, &mapz, sm, s, i0, j0, k0);
     double acc[3][Q];
 #pragma unroll
     for (int d = 0; d < 3; ++d)
@@ -119,8 +127,8 @@ k_sn_scan(SnGeo g, const __grid_constant__ NodeTab tab, const __grid_constant__ 
     const size_t QS = (size_t)Q * g.S, k = (size_t)k0 + lane;
     for (int s = 0; s <= g.nz + 1; ++s) {
         if (s <= g.nz) {
-            const int nb = s % kStNB;
-            st_mbar_wait(&sm.full[nb], (unsigned)((s / kStNB) & 1));
+            const int nb = s % kSnNB;
+            st_mbar_wait(&sm.full[nb], (unsigned)((s / kSnNB) & 1));
             if (ok) {
                 const double *v = sm.buf[nb] + ow;
                 if (inner_pencil && s >= 2 && s <= g.nz - 2) {
@@ -137,8 +145,8 @@ k_sn_scan(SnGeo g, const __grid_constant__ NodeTab tab, const __grid_constant__ 
         if (s >= 1 && ok) {
             const int l = s - 1;
             const size_t row = (size_t)i + (size_t)(g.nx + 1) * (j + (size_t)(g.ny + 1) * l);
-            const double *own = sm.buf[(s + kStNB - 1) % kStNB] + oo;
-            const double inv = omega_n / __ldg(dN + row);
+            const double *own = sm.buf[(s + kSnNB - 1) % kSnNB] + oo;
+            const double inv = omega_n * tab.dinv[9 * ci + 3 * cj + st_cls(l, g.nz)];   // omega_n / d_n
             double z2[Q], u[Q];
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
@@ -172,8 +180,8 @@ k_sn_scan(SnGeo g, const __grid_constant__ NodeTab tab, const __grid_constant__ 
             acc[2][q] = 0.0;
         }
         // last-arriver refill of the buffer of level s-1 (stencil.cuh, st_release)
-        if (s >= 1 && s - 1 + kStNB <= g.nz && st_release<Tl::Warps>(&sm.done[(s - 1) % kStNB]) && lane == 0)
-            sn_stage<Q, Tl>(g, &mapz, sm, s - 1 + kStNB, i0, j0, k0);
+        if (s >= 1 && s - 1 + kSnNB <= g.nz && st_release<Tl::Warps>(&sm.done[(s - 1) % kSnNB]) && lane == 0)
+            sn_stage<Q, Tl>(g, &mapz, sm, s - 1 + kSnNB, i0, j0, k0);
     }
 }
 

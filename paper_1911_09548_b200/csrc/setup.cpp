@@ -683,6 +683,7 @@ bool build_node_tab(const HostLevel &L, NodeTab &tab) {
             if (i + di < 0 || i + di > nx || j + dj < 0 || j + dj > ny || l + dl < 0 || l + dl > nz) return false;
         }
     }
+    for (int c = 0; c < kSnClasses; ++c) tab.dinv[c] = tab.c[c][13] != 0.0 ? 1.0 / tab.c[c][13] : 0.0;
     return true;
 }
 

@@ -1,6 +1,5 @@
-for k in k_sn_scan k_prolong k_restrict k_g_update k_gt k_st_residual; do
-  timeout 300 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o /tmp/n_$k python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-  ncu -i /tmp/n_$k.ncu-rep --page raw --csv > gpurun_out/s6_raw_$k.csv 2>&1
-  ncu -i /tmp/n_$k.ncu-rep --page source --csv --print-source sass > gpurun_out/s6_src_$k.csv 2>&1
-done
-ls -la gpurun_out/ | tail -14
+timeout 300 python bench.py --no-cpu-baseline > gpurun_out/s8_bench.json 2> gpurun_out/s8_bench.err; echo bench_rc=$?
+python -c "
+import json;d=json.load(open('gpurun_out/s8_bench.json'));n=d['kernels']['coarsest']['launches'];print(d['ms_per_step'], d['value']/1e9, d['roofline']['achieved'], d['roofline']['frac']); print({k:round(v['ms']/n,2) for k,v in d['kernels'].items()}); print(d['e2e'])"
+timeout 1500 python -m pytest tests/test_gpu_stencil.py tests/test_gpu_bench_paths.py tests/test_gpu_parity.py tests/test_gpu_edgecases.py tests/test_gpu_distributed.py tests/test_gpu_inner_mg.py tests/test_gpu_fullsize.py -q -x -p no:cacheprovider > gpurun_out/s8_t.log 2>&1; echo t_rc=$?
+tail -5 gpurun_out/s8_t.log
