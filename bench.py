@@ -265,7 +265,7 @@ def run_ours(args, rank, world, local_rank):
                 # ||r||, one V-cycle, ||r||, D2H x; the copies of neighbouring steps overlap the solve
                 xh2 = torch.zeros(fh.shape, dtype=torch.float64).pin_memory()
                 s.solve_many_host([xh.numpy()], [fh.numpy()], tol=0.0, maxit=1, history=False)   # warm-up
-                ke = max(2, args.steps)              # two pinned output buffers, reused alternately
+                ke = max(20, args.steps)             # two pinned output buffers, reused alternately
                 outs = [(xh if i % 2 == 0 else xh2).numpy() for i in range(ke)]
                 t0 = time.perf_counter()
                 s.solve_many_host(outs, [fh.numpy()] * ke, tol=0.0, maxit=1, history=False)
