@@ -132,8 +132,8 @@ struct DevLevel {
     bool use_march = false;
     bool use_stencil = false;       // structured stencil march (stencil.cuh) for residual and sweep
     StencilTab *st_tab = nullptr;   // host copy of the level's stencil table (owned by the handle)
-    double *st_cpl = nullptr;       // [chunk][row] upwind coupling of each 32-slab chunk's first slab
-    double *st_bslab = nullptr;     // [chunk][row] x_q of the slab before each chunk (k_st_bslab)
+    double *st_cpl = nullptr;       // [row][chunk] upwind coupling of each 32-slab chunk's first slab
+    double *st_bslab = nullptr;     // [row][chunk] x_q of the slab before each chunk (k_st_bslab)
     NodeTab *sn_tab = nullptr;      // host copy of the level's node stencil table (structured node scan), or null
     double *sn_ctot = nullptr;      // [chunk][node] Sigma_t chunk totals (k_sn_scan)
     double *sn_cc = nullptr;        // [chunk][node] chunk carries (k_sn_carry), added by the G update

@@ -1409,9 +1409,8 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
             const double *cpl = nullptr;
             if (g.n_chunks > 1 || prev) {
                 const long long n = (long long)L.n_edges * g.n_chunks;
-                if (L.M.width > 9) throw std::logic_error("stencil coupling: mass ELL wider than 9");
                 k_st_bslab<QQ><<<nblocks(n), kBlock, 0, st>>>(L.n_edges, L.S, g.n_chunks, x, prev, L.st_bslab);
-                k_st_coupling<<<nblocks(L.n_edges), kBlock, 0, st>>>(L.n_edges, g.n_chunks, L.M, L.st_bslab, L.st_cpl);
+                k_st_coupling<<<nblocks(n), kBlock, 0, st>>>(L.n_edges, g.n_chunks, L.M, L.st_bslab, L.st_cpl);
                 g_extra_launches += 2;
                 cpl = L.st_cpl;
             }
