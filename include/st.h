@@ -218,7 +218,9 @@ int st_host_matrix(const st_params *p, int level, int which, int *rows, int *wid
 
 /* Diagnostics: bit i of *mask (host) is set when the kernel variant st_variant_name(i) (e.g.
  * "sweep/spl4": the block-Jacobi sweep at 4 slabs per lane; "node_scan/multichunk": the Sigma_t
- * scan carrying over several slab chunks) has been launched by this process since the last
+ * scan carrying over several slab chunks; "stencil/residual", "stencil/sweep",
+ * "stencil/node_scan": the TMA-staged structured marches of uniform hex levels) has been
+ * launched by this process since the last
  * reset; reset != 0 clears the log after reading.  Lets tests prove which code paths ran.
  * st_variant_name returns NULL past the last variant. */
 int st_kernel_variants(uint64_t *mask, int reset);

@@ -265,6 +265,17 @@ double *inner_vcycle(st_handle *h, std::vector<DevLevel> &V, int j, const double
     return cur;
 }
 
+// what the driver knows about the level's x after a kernel wrote it (DevLevel::xs): the stencil
+// sweep / G update / prolongation leave the chunk boundary slabs of x in L.st_bslab
+static void x_written(st_handle *h, DevLevel &L, const double *x, bool producer) {
+    L.xs = producer && st::bslab_producer(L, h->Q) ? st::XS_BSLAB : st::XS_UNKNOWN;
+    L.xs_ptr = x;
+}
+static void x_unknown(DevLevel &L) {
+    L.xs = st::XS_UNKNOWN;
+    L.xs_ptr = nullptr;
+}
+
 void smooth_S(st_handle *h, DevLevel &L, double *x, const double *f, const double *prev) {
     const auto &o = h->o;
     if (o.inner == 1 && L.inner_id >= 0) {
@@ -275,6 +286,7 @@ void smooth_S(st_handle *h, DevLevel &L, double *x, const double *f, const doubl
             st::launch_residual((st::Stream)h->stream, L, h->kt, h->Q, x, f, prev, V[0].r, V[0].z, o.omega_in, nullptr);
         });
         inner_vcycle(h, V, 0, V[0].r, x);
+        x_written(h, L, x, false);
         return;
     }
     auto s = (st::Stream)h->stream;
@@ -283,6 +295,7 @@ void smooth_S(st_handle *h, DevLevel &L, double *x, const double *f, const doubl
     if (o.nu_s == 1) {
         h->run("residual", 3 * ev + ob, 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, prev, nullptr, L.z, o.omega_s, nullptr); });
         h->run("axpy", 3 * ev, 1, [&] { st::launch_axpy(s, vec_len(L, Q), o.omega, L.z, x); });
+        x_written(h, L, x, false);
         return;
     }
     h->run("residual", (o.nu_s > 2 ? 4 : 3) * ev + ob, 1, [&] {
@@ -296,6 +309,7 @@ void smooth_S(st_handle *h, DevLevel &L, double *x, const double *f, const doubl
     h->run("sweep_update", (o.nu_s == 2 ? 3 : 4) * ev + ob, 1, [&] {
         st::launch_sweep(s, L, h->kt, Q, true, o.nu_s == 2, cur, L.r, x, o.omega_s, o.omega);
     });
+    x_written(h, L, x, true);
 }
 
 // first half of the nodal correction: r, G^T r, nodal sweeps and the local time scan into L.y;
@@ -341,6 +355,7 @@ void correct_A_apply(st_handle *h, DevLevel &L, double *x, const double *carry) 
     const int Q = h->Q;
     h->run("g_update", 2 * evec(L, Q) + nvec(L, Q) + 8.0 * L.n_edges, 1,
            [&] { st::launch_g_update(s, L, h->kt, Q, L.y, carry, L.sn_pending ? L.sn_cc : nullptr, x); });
+    x_written(h, L, x, true);
 }
 
 void correct_A(st_handle *h, DevLevel &L, double *x, const double *f, const double *prev) {
@@ -369,6 +384,7 @@ void prolong_from(st_handle *h, DevLevel &L, DevLevel &C, const double *xc, doub
     const int Q = h->Q;
     h->run("prolong", 2 * evec(L, Q) + evec(C, Q) + (L.space_coarsened ? ell_bytes(L.Pg) : 0.0), 1,
            [&] { st::launch_prolong(s, L, Q, xc, x); });
+    x_written(h, L, x, true);
 }
 
 // single-process V-cycle over the level vector V from level l (the last entry is the coarsest)
@@ -379,13 +395,18 @@ void vcycle(st_handle *h, std::vector<DevLevel> &V, int l, double *x, const doub
     if (l == (int)V.size() - 1) {
         const double N = (double)Q * L.n_edges;
         h->run("coarsest", L.S * (N * N * 8.0 + 2 * evec(L, Q) / L.S), L.S, [&] { st::launch_coarsest(s, L, Q, f, x); });
+        x_written(h, L, x, false);
         return;
     }
     hybrid(h, L, x, f, true);
     DevLevel &C = V[l + 1];
     h->run("residual", 3 * evec(L, Q) + op_bytes(L), 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, nullptr, L.r, nullptr, h->o.omega_s, nullptr); });
     restrict_to(h, L, C, L.r, C.f);
-    if (l + 1 < (int)V.size() - 1) ck(cudaMemsetAsync(C.x, 0, sizeof(double) * vec_len(C, Q), h->stream), "memset");
+    if (l + 1 < (int)V.size() - 1) {
+        ck(cudaMemsetAsync(C.x, 0, sizeof(double) * vec_len(C, Q), h->stream), "memset");
+        C.xs = st::XS_ZERO;         // the first residual of the coarse level needs no chunk coupling
+        C.xs_ptr = C.x;
+    }
     vcycle(h, V, l + 1, C.x, C.f);
     prolong_from(h, L, C, C.x, x);
     hybrid(h, L, x, f, false);
@@ -393,6 +414,7 @@ void vcycle(st_handle *h, std::vector<DevLevel> &V, int l, double *x, const doub
 
 // the single-process V-cycle on the finest level, through a captured CUDA graph when enabled
 void run_vcycle(st_handle *h, double *x, const double *f) {
+    x_unknown(h->dl[0]);            // the caller may have changed x since the last V-cycle
     if (!h->use_graphs || h->prof || h->debug_sync) { vcycle(h, h->dl, 0, x, f); return; }
     for (auto &g : h->graphs)
         if (g.x == x && g.f == f) {
@@ -750,6 +772,7 @@ int st_residual(st_handle *h, const double *x, const double *f, double *r, doubl
     ST_CHECK_ALIGNED(x, f, r);
     ST_GUARD({
         DevLevel &L = h->dl[0];
+        x_unknown(L);               // the caller may have changed x since the last call
         auto s = (st::Stream)h->stream;
         if (r) {
             st::launch_residual(s, L, h->kt, h->Q, x, f, nullptr, r, nullptr, h->o.omega_s, nullptr);
@@ -784,6 +807,7 @@ int st_solve(st_handle *h, double *x, const double *f, double tol, int maxit, in
     ST_CHECK_ALIGNED(x, f);
     if (h->nranks > 1) return fail(1, "multi-rank handles solve through paper_1911_09548_b200.distributed");
     ST_GUARD({
+        x_unknown(h->dl[0]);
         if (tol <= 0.0 && !hist) {
             // no stopping test and no history requested: exactly maxit V-cycles, no norms
             for (int it = 0; it < maxit; ++it) run_vcycle(h, x, f);
@@ -997,6 +1021,7 @@ int st_lv_residual(st_handle *h, int set, int level, const double *x, const doub
     ST_CHECK_ALIGNED(x, f, r);
     ST_GUARD({
         DevLevel &L = level_of(h, set, level);
+        x_unknown(L);               // level operations: the driver moves x between calls
         auto s = (st::Stream)h->stream;
         const int Q = h->Q;
         if (r) h->run("residual", 3 * evec(L, Q) + op_bytes(L), 1, [&] { st::launch_residual(s, L, h->kt, Q, x, f, prev, r, nullptr, h->o.omega_s, nullptr); });
@@ -1014,13 +1039,21 @@ int st_lv_residual(st_handle *h, int set, int level, const double *x, const doub
 int st_lv_smooth_S(st_handle *h, int set, int level, double *x, const double *f, const double *prev) {
     if (!h || !x || !f) return fail(1, "null argument");
     ST_CHECK_ALIGNED(x, f);
-    ST_GUARD(smooth_S(h, level_of(h, set, level), x, f, prev))
+    ST_GUARD({
+        DevLevel &L = level_of(h, set, level);
+        x_unknown(L);
+        smooth_S(h, L, x, f, prev);
+    })
 }
 
 int st_lv_correct_local(st_handle *h, int set, int level, double *x, const double *f, const double *prev, double *tot) {
     if (!h || !x || !f) return fail(1, "null argument");
     ST_CHECK_ALIGNED(x, f);
-    ST_GUARD(correct_A_local(h, level_of(h, set, level), x, f, prev, tot))
+    ST_GUARD({
+        DevLevel &L = level_of(h, set, level);
+        x_unknown(L);
+        correct_A_local(h, L, x, f, prev, tot);
+    })
 }
 
 int st_lv_correct_apply(st_handle *h, int set, int level, double *x, const double *carry) {
@@ -1056,6 +1089,7 @@ int st_lv_vcycle(st_handle *h, int set, int level, double *x, const double *f) {
         auto &V = level_set(h, set);
         if (V.back().Ainv == nullptr) throw std::invalid_argument("this level set has no coarsest level");
         if (level < 0 || level >= (int)V.size()) throw std::invalid_argument("level out of range");
+        x_unknown(V[level]);
         vcycle(h, V, level, x, f);
     })
 }

@@ -117,6 +117,8 @@ struct Grid3 {
     const double *sigma, *nu;
 };
 
+enum XState { XS_UNKNOWN = 0, XS_ZERO = 1, XS_BSLAB = 2 };
+
 struct DevLevel {
     int n_edges = 0, n_nodes = 0, S = 0, Q = 1;
     DevELL M, K, Kn, GT, Pg, Rg, GtM;
@@ -138,6 +140,11 @@ struct DevLevel {
     double *sn_ctot = nullptr;      // [chunk][node] Sigma_t chunk totals (k_sn_scan)
     double *sn_cc = nullptr;        // [chunk][node] chunk carries (k_sn_carry), added by the G update
     bool sn_pending = false;        // the last node scan left its chunk carries for the G update
+    // what the V-cycle driver (api.cpp) knows about x = xs_ptr on this level: nothing, x = 0, or
+    // st_bslab holds x_q of every chunk's last slab (side output of the sweep / G update /
+    // prolongation that last wrote x); the residual's chunk coupling then skips k_st_bslab
+    int xs = 0;
+    const double *xs_ptr = nullptr;
     int lpr_log2 = 5;       // edge kernels: log2(lanes per row); slab chunk = 2 << lpr_log2 (32: measured best)
     Grid3 grid{};
     double *tau = nullptr;
@@ -185,6 +192,9 @@ void launch_gtr(Stream st, const DevLevel &L, const KT &kt, int Q, const double 
                 double omega_n, double *zn, double *w);
 void launch_node_sweep(Stream st, const DevLevel &L, int Q, const double *z, const double *w, double omega_n,
                        double *zout);
+// true when the sweep (last), the G update and the prolongation of this level write the chunk
+// boundary slabs of x into L.st_bslab as a side output
+bool bslab_producer(const DevLevel &L, int Q);
 // returns true when it left chunk carries (L.sn_cc) that the G update of this level must add
 bool launch_node_scan(Stream st, const DevLevel &L, const KT &kt, int Q, int mode, const double *z,
                       const double *w, double omega_n, const double *carry, double *y, double *tot);

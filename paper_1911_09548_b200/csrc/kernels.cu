@@ -40,7 +40,7 @@ static const char *const kVariantNames[] = {
     "sweep/chunked", "res_mass/spl1", "res_mass/spl2", "res_mass/spl4", "res_mass/chunked",
     "gtr/fused", "gtr/chunked", "gt/two-pass", "node_scan/multichunk", "node_scan/carry-in",
     "march/residual", "march/sweep", "restrict/space", "prolong/space", "stencil/residual",
-    "stencil/sweep", "stencil/res_mass", "coupling/prev", "stencil/node_scan"};
+    "stencil/sweep", "stencil/res_mass", "coupling/prev", "stencil/node_scan", "coupling/side-output"};
 constexpr int kNumVariants = (int)(sizeof(kVariantNames) / sizeof(kVariantNames[0]));
 static std::atomic<unsigned long long> g_variants{0};
 static inline void note(int bit) { g_variants.fetch_or(1ull << bit, std::memory_order_relaxed); }
@@ -49,7 +49,7 @@ enum VariantBit {
     V_SWEEP_SPL1, V_SWEEP_SPL2, V_SWEEP_SPL4, V_SWEEP_CHUNKED, V_RM_SPL1, V_RM_SPL2, V_RM_SPL4, V_RM_CHUNKED,
     V_GTR_FUSED, V_GTR_CHUNKED, V_GT_TWOPASS, V_SCAN_MULTI, V_SCAN_CARRY, V_MARCH_RES, V_MARCH_SWEEP,
     V_RESTRICT_SPACE, V_PROLONG_SPACE, V_STENCIL_RES, V_STENCIL_SWEEP, V_STENCIL_RM, V_COUPLING_PREV,
-    V_SN_SCAN
+    V_SN_SCAN, V_BSLAB_SIDE
 };
 unsigned long long variants(bool reset) {
     return reset ? g_variants.exchange(0) : g_variants.load();
@@ -809,7 +809,8 @@ __global__ void __launch_bounds__(kBlock) k_node_scan(int nodes, int S, DevELL K
 template <int Q, int SPL>
 __global__ void __launch_bounds__(kBlock) k_g_update(BoxMap m, const int *__restrict__ en, const double *__restrict__ y,
                                                      const double *__restrict__ carry, const double *__restrict__ cc,
-                                                     int n_nodes, KT kt, double *__restrict__ x) {
+                                                     int n_nodes, KT kt, double *__restrict__ x, double *__restrict__ bslab,
+                                                     int n_edges) {
     box_loop(m, [&](int e, int k0, bool valid) {
     if (!valid) return;
     const int S = m.S;
@@ -829,6 +830,9 @@ __global__ void __launch_bounds__(kBlock) k_g_update(BoxMap m, const int *__rest
 #pragma unroll
         for (int j = 0; j < SPL; ++j) xv[j] += y1[j] - y0[j] + kt.g[a] * dc;
         stv<SPL>(x + e * QS + a * S + k0, xv);
+        // side output: x_q of the last slab of a 32-slab chunk, for the next chunk's coupling
+        if (bslab && a == Q - 1 && (k0 + SPL) % 32 == 0 && k0 + SPL < S)
+            bslab[(size_t)((k0 + SPL) / 32) * n_edges + e] = xv[SPL - 1];
     }
 });
 }
@@ -1131,7 +1135,8 @@ __global__ void __launch_bounds__(kBlock) k_restrict(Map m, DevELL Rg, const dou
 // one thread per (fine row, coarse slab K) writing the fine slab pair as one 16-byte store.
 template <int Q, bool SPACE>
 __global__ void __launch_bounds__(kBlock) k_prolong(Map m, DevELL Pg, const double *__restrict__ xc,
-                                                    const double *__restrict__ Pt, double *__restrict__ x) {
+                                                    const double *__restrict__ Pt, double *__restrict__ x,
+                                                    double *__restrict__ bslab, int n_edges) {
     __shared__ double Ps[2 * Q * Q][32];
     stage_pt<Q>(m, Pt, Ps);
     int rf, K;
@@ -1163,6 +1168,9 @@ __global__ void __launch_bounds__(kBlock) k_prolong(Map m, DevELL Pg, const doub
         double2 xv = *px;
         xv.x += t0; xv.y += t1;
         *px = xv;
+        // side output: x_q of a chunk's last slab (fine slab 2K + 1 = 32c - 1) for the coupling
+        if (bslab && b == Q - 1 && (2 * K + 2) % 32 == 0 && 2 * K + 2 < S)
+            bslab[(size_t)((2 * K + 2) / 32) * n_edges + rf] = xv.y;
     }
 }
 
@@ -1306,6 +1314,8 @@ bool stencil_applies(const DevLevel &L, int Q) {
     return L.use_stencil && L.st_tab && (Q == 1 || Q == 2) && L.S % kStSPW == 0;
 }
 
+bool bslab_producer(const DevLevel &L, int Q) { return stencil_applies(L, Q) && L.st_bslab; }
+
 
 static Map make_map(int rows, int S, bool allow_pairs = true) {
     Map m{};
@@ -1406,12 +1416,26 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
         ST_DISPATCH_Q12(Q, {
             // the upwind coupling of every chunk's first slab: one small gather pass (9 mass
             // entries per row and chunk) before the march
+            // the upwind coupling of every chunk's first slab (k_st_coupling): nothing when x = 0 and
+            // there is no previous rank; the slab before each chunk from the side output of the
+            // kernel that last wrote x when api.cpp vouches for it (L.xs), else from k_st_bslab
             const double *cpl = nullptr;
-            if (g.n_chunks > 1 || prev) {
+            const bool zero = L.xs == XS_ZERO && L.xs_ptr == x;
+            if ((g.n_chunks > 1 && !zero) || prev) {
+                const bool have_b = zero || (L.xs == XS_BSLAB && L.xs_ptr == x);
+                if (!have_b) {
+                    const long long nb1 = (long long)L.n_edges * (g.n_chunks - 1);
+                    if (nb1 > 0) {
+                        k_st_bslab<QQ><<<nblocks(nb1), kBlock, 0, st>>>(L.n_edges, L.S, g.n_chunks, x, L.st_bslab);
+                        ++g_extra_launches;
+                    }
+                } else {
+                    note(V_BSLAB_SIDE);
+                }
                 const long long n = (long long)L.n_edges * g.n_chunks;
-                k_st_bslab<QQ><<<nblocks(n), kBlock, 0, st>>>(L.n_edges, L.S, g.n_chunks, x, prev, L.st_bslab);
-                k_st_coupling<<<nblocks(n), kBlock, 0, st>>>(L.n_edges, g.n_chunks, L.M, L.st_bslab, L.st_cpl);
-                g_extra_launches += 2;
+                k_st_coupling<<<nblocks(n), kBlock, 0, st>>>(L.n_edges, g.n_chunks, L.M, zero ? nullptr : L.st_bslab,
+                                                             prev, L.st_cpl);
+                ++g_extra_launches;
                 cpl = L.st_cpl;
             }
             StMaps maps;
@@ -1493,7 +1517,8 @@ void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, 
             stencil_maps<QQ, Tl>(L, z, maps);
             auto launch = [&](auto kern) {
                 stencil_smem_attr(kern, (int)sm);
-                kern<<<nb, nt, sm, st>>>(g, *L.st_tab, maps, L.tau, r, out, omega_s, omega, kt);
+                kern<<<nb, nt, sm, st>>>(g, *L.st_tab, maps, L.tau, r, out, omega_s, omega, kt,
+                                         last ? L.st_bslab : nullptr);
             };
             if (last && recon) launch(k_st_sweep<QQ, true, true>);
             else if (last) launch(k_st_sweep<QQ, true, false>);
@@ -1653,8 +1678,9 @@ void launch_g_update(Stream st, const DevLevel &L, const KT &kt, int Q, const do
                      const double *cc, double *x) {
     const BoxMap m = edge_map(L);
     if (cc && (m.chunk % kStSPW != 0 && m.S > m.chunk)) throw std::logic_error("g_update: lane slabs straddle a chunk");
+    double *bs = bslab_producer(L, Q) ? L.st_bslab : nullptr;
     ST_DISPATCH_Q(Q, ST_DISPATCH_SPL(m.spl, k_g_update<QQ, SP><<<grid(m), kBlock, 0, st>>>(m, L.edge_nodes, y, carry, cc,
-                                                                                            L.n_nodes, kt, x)));
+                                                                                            L.n_nodes, kt, x, bs, L.n_edges)));
 }
 
 void launch_copy_slabs(Stream st, int rows, int Q, int ns, double *dst, int dS, int dk0, const double *src, int sS,
@@ -1680,8 +1706,9 @@ void launch_prolong(Stream st, const DevLevel &F, int Q, const double *xc, doubl
     const Map m = make_map(F.n_edges, F.S / 2, false);
     if (F.space_coarsened) note(V_PROLONG_SPACE);
     ST_DISPATCH_Q(Q, {
-        if (F.space_coarsened) k_prolong<QQ, true><<<grid(m), kBlock, 0, st>>>(m, F.Pg, xc, F.Pt, x);
-        else k_prolong<QQ, false><<<grid(m), kBlock, 0, st>>>(m, F.Pg, xc, F.Pt, x);
+        double *bs = bslab_producer(F, Q) ? F.st_bslab : nullptr;
+        if (F.space_coarsened) k_prolong<QQ, true><<<grid(m), kBlock, 0, st>>>(m, F.Pg, xc, F.Pt, x, bs, F.n_edges);
+        else k_prolong<QQ, false><<<grid(m), kBlock, 0, st>>>(m, F.Pg, xc, F.Pt, x, bs, F.n_edges);
     });
 }
 

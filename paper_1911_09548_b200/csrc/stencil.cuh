@@ -494,15 +494,14 @@ struct StResOp {
     size_t bstride;
     double omega_s;
     bool first;                     // lane of the chunk's first slab
-    const double *cpl;              // (M x_q) of the slab before this chunk: cpl[row * n_chunks] (k_st_coupling), or null
-    int n_chunks;
+    const double *cpl;              // (M x_q) of the slab before this chunk, per row (k_st_coupling), or null
     double nrm;
     double fv[3][Q], cv[3];
     __device__ __forceinline__ void pre(int T, unsigned row, const double *) {
         const char *p = fb + (size_t)row * rowbytes;
 #pragma unroll
         for (int b = 0; b < Q; ++b) fv[T][b] = __ldg(reinterpret_cast<const double *>(p + b * bstride));
-        cv[T] = first && cpl ? __ldg(cpl + (size_t)row * n_chunks) : 0.0;     // null: chunk 0, zero initial state
+        cv[T] = first && cpl ? __ldg(cpl + row) : 0.0;     // null: no coupling (zero initial state, x = 0)
     }
     template <bool FAST>
     __device__ __forceinline__ void emit(int T, unsigned row, int cls, const double (&m)[Q], const double (&k)[Q]) {
@@ -534,7 +533,7 @@ struct StResOp {
     }
 };
 
-// cpl: the coupling of each chunk's first slab from k_st_coupling ([row][chunk]), or null when there
+// cpl: the coupling of each chunk's first slab from k_st_coupling ([chunk][row]), or null when there
 // is none (a single chunk and the zero initial state)
 template <int Q, bool R_OUT, bool Z_OUT, bool NORM, class Tl = StTileRes>
 __global__ void __launch_bounds__(32 * Tl::Warps, 1)
@@ -554,7 +553,9 @@ k_st_residual(StGeo g, const __grid_constant__ StencilTab tab, const __grid_cons
                                            reinterpret_cast<char *>(r) + lane_off,
                                            reinterpret_cast<char *>(z) + lane_off, rowbytes, (size_t)g.S * 8, omega_s,
                                            (threadIdx.x & 31) == 0,
-                                           cpl ? cpl + chunk : nullptr, g.n_chunks, 0.0, {}, {}};
+                                           cpl ? cpl + (size_t)chunk * (g.Ex + g.Ey + (size_t)(g.nx + 1) * (g.ny + 1) * g.nz)
+                                               : nullptr,
+                                           0.0, {}, {}};
     st_march<Q, Tl, false>(g, tab, maps, sm, tile, chunk, op);
     if (NORM) {
         __shared__ double sh[Tl::Warps];
@@ -576,6 +577,7 @@ struct StSweepOp {
     unsigned rowbytes;
     size_t bstride;
     double omega_s, omega;
+    double *bsl;                    // LAST: x_q of this lane's slab for the next chunk's coupling (lane 31), or null
     double zv[3][Q], rv[3][Q], xv[3][Q];
     __device__ __forceinline__ void pre(int T, unsigned row, const double *own) {
         const size_t off = (size_t)row * rowbytes;
@@ -603,8 +605,13 @@ struct StSweepOp {
             for (int a = 0; a < Q; ++a) y = fma(Di[b * Q + a], d[a], y);
             const double res = RECON ? fma(-omega_s, y, 2.0 * zv[T][b]) : fma(omega_s, y, zv[T][b]);
             double *o = reinterpret_cast<double *>(ob + off + b * bstride);
-            if (LAST) *o = fma(omega, res, xv[T][b]);
-            else *o = res;
+            if (LAST) {
+                const double xn = fma(omega, res, xv[T][b]);
+                *o = xn;
+                if (b == Q - 1 && bsl) bsl[row] = xn;       // the chunk's last slab (lane 31 only)
+            } else {
+                *o = res;
+            }
         }
     }
 };
@@ -613,7 +620,7 @@ template <int Q, bool LAST, bool RECON, class Tl = StTileSweep>
 __global__ void __launch_bounds__(32 * Tl::Warps, 1)
 k_st_sweep(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constant__ StMaps maps,
            const double *__restrict__ tau, const double *__restrict__ r, double *out, double omega_s, double omega,
-           KT kt) {
+           KT kt, double *__restrict__ bslab) {
     extern __shared__ __align__(128) unsigned char st_dyn[];
     StSmem<Q, Tl> &sm = *reinterpret_cast<StSmem<Q, Tl> *>(st_dyn + ((128u - (st_smem_addr(st_dyn) & 127u)) & 127u));
     __shared__ StBlockTab<Q> bt;
@@ -623,41 +630,47 @@ k_st_sweep(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constan
     st_block_table<Q>(tab, kt, L, bt);
     const unsigned rowbytes = (unsigned)(8u * Q * g.S);
     const size_t lane_off = (size_t)L.k * 8;
+    // LAST: lane 31 holds the slab before chunk + 1; it records x_q there for that chunk's coupling
+    // (bslab[(chunk + 1) * n_edges + row], the layout of k_st_bslab)
+    const size_t n_edges = (size_t)g.Ex + g.Ey + (size_t)(g.nx + 1) * (g.ny + 1) * g.nz;
+    double *bsl = (LAST && bslab && (threadIdx.x & 31) == 31 && chunk + 1 < g.n_chunks)
+                      ? bslab + (size_t)(chunk + 1) * n_edges : nullptr;
     StSweepOp<Q, LAST, RECON> op{tab, kt, L, bt, reinterpret_cast<const char *>(r) + lane_off,
                                  reinterpret_cast<char *>(out) + lane_off, rowbytes, (size_t)g.S * 8, omega_s, omega,
-                                 {}, {}, {}};
+                                 bsl, {}, {}, {}};
     st_march<Q, Tl, true>(g, tab, maps, sm, tile, chunk, op);
 }
 
 // The upwind coupling of each chunk's first slab (N_t = e_0 e_q^T): (M x_q) of the
-// slab before the chunk (chunk c >= 1: slab 32c - 1; chunk 0: the previous rank's end values `prev`),
-// out[row * n_chunks + c].  Two passes so that x is touched once per (column, chunk): k_st_bslab
-// copies x_q(32c - 1) of every row into a compact [row][chunk] array, then k_st_coupling applies the
-// 9-slot mass ELL to it.  Threads run over (row, chunk) with the chunk fastest: the 16 strided reads
-// of one row fall in one 4 KB stretch of it (DRAM page locality: measured 0.276 ms per c4 launch
-// with the chunk-major order, one sector per row 8 KB apart), and every store is coalesced.
+// slab before the chunk (chunk c >= 1: slab 32c - 1; chunk 0: the previous rank's end values `prev`,
+// or nothing), out[c * n_edges + row].  The values x_q(32c - 1) come from a compact [chunk][row]
+// array b: written as a side output by the kernels that last wrote x (the stencil sweep, the G
+// update, the prolongation: api.cpp tracks for which x it is current), else copied by k_st_bslab
+// (one strided 8-byte read per value).  k_st_coupling applies the 9-slot mass ELL to it.
 template <int Q>
 __global__ void __launch_bounds__(256) k_st_bslab(int n_edges, int S, int n_chunks, const double *__restrict__ x,
-                                                   const double *__restrict__ prev, double *__restrict__ b) {
-    const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+                                                   double *__restrict__ b) {
+    const long long id = (long long)n_edges + blockIdx.x * (long long)blockDim.x + threadIdx.x;   // chunks >= 1
     if (id >= (long long)n_edges * n_chunks) return;
-    const int row = (int)(id / n_chunks), c = (int)(id - (long long)row * n_chunks);
-    b[id] = c == 0 ? (prev ? __ldg(prev + row) : 0.0)
-                   : __ldg(x + (size_t)row * Q * S + (size_t)(Q - 1) * S + (size_t)c * kStSPW - 1);
+    const int c = (int)(id / n_edges), row = (int)(id - (long long)c * n_edges);
+    b[id] = __ldg(x + (size_t)row * Q * S + (size_t)(Q - 1) * S + (size_t)c * kStSPW - 1);
 }
 
 __global__ void __launch_bounds__(256) k_st_coupling(int n_edges, int n_chunks, DevELL M, const double *__restrict__ b,
-                                                      double *__restrict__ out) {
+                                                      const double *__restrict__ prev, double *__restrict__ out) {
     const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (id >= (long long)n_edges * n_chunks) return;
-    const int row = (int)(id / n_chunks), c = (int)(id - (long long)row * n_chunks);
-    const Ent *e = M.e + (size_t)row * M.width;
+    const int c = (int)(id / n_edges), row = (int)(id - (long long)c * n_edges);
+    const double *src = c == 0 ? prev : b + (size_t)c * n_edges;
     double acc = 0.0;
-    for (int s = 0; s < M.width; ++s) {
-        double v;
-        int col;
-        ld_ent(e + s, v, col);
-        acc = fma(v, __ldg(b + (size_t)col * n_chunks + c), acc);
+    if (src) {
+        const Ent *e = M.e + (size_t)row * M.width;
+        for (int s = 0; s < M.width; ++s) {
+            double v;
+            int col;
+            ld_ent(e + s, v, col);
+            acc = fma(v, __ldg(src + col), acc);
+        }
     }
     out[id] = acc;
 }
