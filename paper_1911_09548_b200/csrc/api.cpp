@@ -298,9 +298,15 @@ void smooth_S(st_handle *h, DevLevel &L, double *x, const double *f, const doubl
         x_written(h, L, x, false);
         return;
     }
-    h->run("residual", (o.nu_s > 2 ? 4 : 3) * ev + ob, 1, [&] {
-        st::launch_residual(s, L, h->kt, Q, x, f, prev, o.nu_s > 2 ? L.r : nullptr, L.z, o.omega_s, nullptr);
-    });
+    if (o.nu_s == 2 && !prev && L.xs == st::XS_ZERO && L.xs_ptr == x) {
+        // x = 0 (a coarse level's first smoothing step): r = f, so the first sweep from zero is the
+        // pointwise z = omega_s D^{-1} f -- no operator pass (the second sweep rebuilds r from z)
+        h->run("residual", 2 * ev, 1, [&] { st::launch_jacobi_point(s, L, h->kt, Q, f, L.z, o.omega_s); });
+    } else {
+        h->run("residual", (o.nu_s > 2 ? 4 : 3) * ev + ob, 1, [&] {
+            st::launch_residual(s, L, h->kt, Q, x, f, prev, o.nu_s > 2 ? L.r : nullptr, L.z, o.omega_s, nullptr);
+        });
+    }
     double *cur = L.z, *other = L.z2;
     for (int i = 2; i < o.nu_s; ++i) {
         h->run("sweep", 3 * ev + ob, 1, [&] { st::launch_sweep(s, L, h->kt, Q, false, false, cur, L.r, other, o.omega_s, o.omega); });
