@@ -1432,9 +1432,9 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
                 } else {
                     note(V_BSLAB_SIDE);
                 }
-                const long long n = (long long)L.n_edges * g.n_chunks;
-                k_st_coupling<<<nblocks(n), kBlock, 0, st>>>(L.n_edges, g.n_chunks, L.M, zero ? nullptr : L.st_bslab,
-                                                             prev, L.st_cpl);
+                if (L.M.width > 9) throw std::logic_error("stencil coupling: mass ELL wider than 9");
+                k_st_coupling<<<nblocks(L.n_edges), kBlock, 0, st>>>(L.n_edges, g.n_chunks, L.M,
+                                                                     zero ? nullptr : L.st_bslab, prev, L.st_cpl);
                 ++g_extra_launches;
                 cpl = L.st_cpl;
             }
