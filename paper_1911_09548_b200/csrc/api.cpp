@@ -63,8 +63,9 @@ struct st_handle {
     int64_t n_dofs = 0;
     // CUDA-graph replay of the single-process V-cycle (st_set_graphs)
     bool use_graphs = false;
-    int nodal_res = 0;          // env ST_NODAL_RES: 0 G^T (f - L x) literally (default), 1 two-pass
-                                // with G^T K = 0 (u = f - Ct M x), 2 fused node-row G^T M (K G = 0)
+    int nodal_res = 3;          // env ST_NODAL_RES: 0 G^T (f - L x) literally, 1 two-pass with
+                                // G^T K = 0 (u = f - Ct M x), 2 fused node-row G^T M (K G = 0),
+                                // 3 (default) the two-pass mass form on stencil levels, 0 elsewhere
     bool mk_dict = true;        // env ST_MK_DICT=0: never use the dictionary ELL
     bool stencil = true;        // env ST_STENCIL=0: never use the structured stencil march
     std::vector<std::unique_ptr<st::StencilTab>> st_tabs;
@@ -210,7 +211,11 @@ size_t vec_len(const DevLevel &L, int Q, bool nodes = false) {
 
 // Algorithmic bytes: every vector touched once, operators read once.
 double ell_bytes(const st::DevELL &E) { return (double)E.rows * E.width * 16.0; }
-double op_bytes(const DevLevel &L) { return ell_bytes(L.M) + ell_bytes(L.K) + 16.0 * L.n_edges; }
+// (stencil levels read no operator: their coefficients are kernel parameters)
+double op_bytes(const DevLevel &L) {
+    if (st::stencil_applies(L, L.Q)) return 0.0;
+    return ell_bytes(L.M) + ell_bytes(L.K) + 16.0 * L.n_edges;
+}
 double evec(const DevLevel &L, int Q) { return 8.0 * L.n_edges * Q * L.S; }
 double nvec(const DevLevel &L, int Q) { return 8.0 * L.n_nodes * Q * L.S; }
 
@@ -325,7 +330,14 @@ void correct_A_local(st_handle *h, DevLevel &L, double *x, const double *f, cons
     auto s = (st::Stream)h->stream;
     const int Q = h->Q;
     const double ev = evec(L, Q), nv = nvec(L, Q), kb = ell_bytes(L.Kn) + 8.0 * L.n_nodes;
-    if (h->nodal_res == 0) {
+    if (h->nodal_res == 3 && st::stencil_applies(L, Q)) {
+        // uniform hex levels (default): the mass form of the same residual, u = f - (Ct (x) M) x +
+        // coupling by the stencil march without its curl-curl part (K G = 0, R17), then
+        // w = G^T u; other levels keep the literal form below
+        h->run("gtr_mass", 3 * ev + op_bytes(L), 1, [&] { st::launch_res_mass(s, L, h->kt, Q, x, f, prev, L.r); });
+        h->run("gt", ev + (o.nu_n > 2 ? 2 : 1) * nv + 8.0 * L.n_nodes, 1,
+               [&] { st::launch_gt(s, L, Q, L.r, o.omega_n, L.zn, o.nu_n > 2 ? L.wn : nullptr); });
+    } else if (h->nodal_res == 0 || h->nodal_res == 3) {
         // Eq. (5) as written: r = f - L x with the full operator, then w = G^T r
         // on node rows (6 gathers).  The K G = 0 shortcuts below are the same map in exact
         // arithmetic but drop G^T K x, which in fp64 is rounding of size eps |tau K x|: measured

@@ -1404,6 +1404,31 @@ static MarchMap march_map(const DevLevel &L, bool halo) {
 }
 static inline int grid(const MarchMap &mm) { return mm.n_pblocks * ((mm.S + mm.stride - 1) / mm.stride); }
 
+// the upwind coupling of every chunk's first slab (k_st_coupling: 9 mass entries per row and chunk),
+// or null: nothing when x = 0 and there is no previous rank; the slab before each chunk from the
+// side output of the kernel that last wrote x when api.cpp vouches for it (L.xs), else from k_st_bslab
+template <int Q>
+static const double *stencil_coupling(Stream st, const DevLevel &L, const StGeo &g, const double *x,
+                                      const double *prev) {
+    const bool zero = L.xs == XS_ZERO && L.xs_ptr == x;
+    if (!((g.n_chunks > 1 && !zero) || prev)) return nullptr;
+    const bool have_b = zero || (L.xs == XS_BSLAB && L.xs_ptr == x);
+    if (!have_b) {
+        const long long nb1 = (long long)L.n_edges * (g.n_chunks - 1);
+        if (nb1 > 0) {
+            k_st_bslab<Q><<<nblocks(nb1), kBlock, 0, st>>>(L.n_edges, L.S, g.n_chunks, x, L.st_bslab);
+            ++g_extra_launches;
+        }
+    } else {
+        note(V_BSLAB_SIDE);
+    }
+    if (L.M.width > 9) throw std::logic_error("stencil coupling: mass ELL wider than 9");
+    k_st_coupling<<<nblocks(L.n_edges), kBlock, 0, st>>>(L.n_edges, g.n_chunks, L.M, zero ? nullptr : L.st_bslab,
+                                                         prev, L.st_cpl);
+    ++g_extra_launches;
+    return L.st_cpl;
+}
+
 int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
                     const double *prev, double *r, double *z, double omega_s, double *partial) {
     if (stencil_applies(L, Q)) {
@@ -1414,30 +1439,7 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
         const int nb = grid(g), nt = 32 * Tl::Warps;
         const size_t sm = Q == 1 ? sizeof(StSmem<1, Tl>) + 128 : sizeof(StSmem<2, Tl>) + 128;
         ST_DISPATCH_Q12(Q, {
-            // the upwind coupling of every chunk's first slab: one small gather pass (9 mass
-            // entries per row and chunk) before the march
-            // the upwind coupling of every chunk's first slab (k_st_coupling): nothing when x = 0 and
-            // there is no previous rank; the slab before each chunk from the side output of the
-            // kernel that last wrote x when api.cpp vouches for it (L.xs), else from k_st_bslab
-            const double *cpl = nullptr;
-            const bool zero = L.xs == XS_ZERO && L.xs_ptr == x;
-            if ((g.n_chunks > 1 && !zero) || prev) {
-                const bool have_b = zero || (L.xs == XS_BSLAB && L.xs_ptr == x);
-                if (!have_b) {
-                    const long long nb1 = (long long)L.n_edges * (g.n_chunks - 1);
-                    if (nb1 > 0) {
-                        k_st_bslab<QQ><<<nblocks(nb1), kBlock, 0, st>>>(L.n_edges, L.S, g.n_chunks, x, L.st_bslab);
-                        ++g_extra_launches;
-                    }
-                } else {
-                    note(V_BSLAB_SIDE);
-                }
-                if (L.M.width > 9) throw std::logic_error("stencil coupling: mass ELL wider than 9");
-                k_st_coupling<<<nblocks(L.n_edges), kBlock, 0, st>>>(L.n_edges, g.n_chunks, L.M,
-                                                                     zero ? nullptr : L.st_bslab, prev, L.st_cpl);
-                ++g_extra_launches;
-                cpl = L.st_cpl;
-            }
+            const double *cpl = stencil_coupling<QQ>(st, L, g, x, prev);
             StMaps maps;
             stencil_maps<QQ, Tl>(L, x, maps);
             auto launch = [&](auto kern) {
@@ -1593,6 +1595,21 @@ void launch_gtr(Stream st, const DevLevel &L, const KT &kt, int Q, const double 
 
 void launch_res_mass(Stream st, const DevLevel &L, const KT &kt, int Q, const double *x, const double *f,
                      const double *prev, double *u) {
+    if (stencil_applies(L, Q)) {
+        note(V_STENCIL_RM);
+        if (prev) note(V_COUPLING_PREV);
+        using Tl = StTileRes;
+        const StGeo g = stencil_geo<Tl>(L);
+        const size_t sm = Q == 1 ? sizeof(StSmem<1, Tl>) + 128 : sizeof(StSmem<2, Tl>) + 128;
+        ST_DISPATCH_Q12(Q, {
+            const double *cpl = stencil_coupling<QQ>(st, L, g, x, prev);
+            StMaps maps;
+            stencil_maps<QQ, Tl>(L, x, maps);
+            stencil_smem_attr(k_st_res_mass<QQ>, (int)sm);
+            k_st_res_mass<QQ><<<grid(g), 32 * Tl::Warps, sm, st>>>(g, *L.st_tab, maps, cpl, f, u, kt);
+        });
+        return;
+    }
     // 4 slabs per lane: measured 68 vs 75 ms per 5 c4 V-cycles at 2 (env ST_RESMASS_SPL)
     static const int spl = std::getenv("ST_RESMASS_SPL") ? std::atoi(std::getenv("ST_RESMASS_SPL")) : 4;
     const BoxMap m = edge_map(L, spl);

@@ -72,7 +72,9 @@ __device__ __forceinline__ void st_phase() {
 
 // xs / ys / zs: the warp's x-, y-, z-edge input blocks of the staged level, element (a, b, q) at
 // [(b * row + a) * Blk + q * 32] with row = the tile-box i extent of the edge type
-template <int Q, class Tl, bool FAST, bool ZIN>
+// MK = false: mass part only (the nodal residual's mass form, k_st_res_mass); the curl-curl FMAs and
+// the inputs only they read are compiled out
+template <int Q, class Tl, bool FAST, bool ZIN, bool MK = true>
 __device__ __forceinline__ void st_push(const StencilTab &tab, const double *xs, const double *ys, const double *zs,
                                         const int (&clsX)[3], const int (&clsY)[3], int clsZ, StAcc<Q> &A) {
     constexpr int Blk = Q * kStSPW;
@@ -98,10 +100,10 @@ __device__ __forceinline__ void st_push(const StencilTab &tab, const double *xs,
 #pragma unroll
                     for (int q = 0; q < Q; ++q) {
                         A.xm[d][q] = fma(c.x, xin[a][b][q], A.xm[d][q]);
-                        A.xk[d][q] = fma(c.y, xin[a][b][q], A.xk[d][q]);
+                        if (MK) A.xk[d][q] = fma(c.y, xin[a][b][q], A.xk[d][q]);
                     }
                 }
-                if (b >= 1) {                                   // Y rows: o = (a-1, b-1, o2)
+                if (MK && b >= 1) {                             // Y rows: o = (a-1, b-1, o2)
                     const double c = st_coef<FAST>(tab, 1, clsY[d], st_slot(1, 0, a - 1, b - 1, o2)).y;
 #pragma unroll
                     for (int q = 0; q < Q; ++q) A.yk[d][q] = fma(c, xin[a][b][q], A.yk[d][q]);
@@ -109,6 +111,7 @@ __device__ __forceinline__ void st_push(const StencilTab &tab, const double *xs,
             }
 #pragma unroll
             for (int e = 0; e < 2; ++e) {                       // Z rows at s-1+e: o = (a-1, b-1, 1-e)
+                if (!MK) break;
                 const double c = st_coef<FAST>(tab, 2, clsZ, st_slot(2, 0, a - 1, b - 1, 1 - e)).y;
 #pragma unroll
                 for (int q = 0; q < Q; ++q) A.zk[e][q] = fma(c, xin[a][b][q], A.zk[e][q]);
@@ -129,7 +132,7 @@ __device__ __forceinline__ void st_push(const StencilTab &tab, const double *xs,
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
                 const int o2 = 1 - d;
-                if (a >= 1) {                                   // X rows: o = (a-1, b-1, o2)
+                if (MK && a >= 1) {                             // X rows: o = (a-1, b-1, o2)
                     const double c = st_coef<FAST>(tab, 0, clsX[d], st_slot(0, 1, a - 1, b - 1, o2)).y;
 #pragma unroll
                     for (int q = 0; q < Q; ++q) A.xk[d][q] = fma(c, yin[a][b][q], A.xk[d][q]);
@@ -139,12 +142,13 @@ __device__ __forceinline__ void st_push(const StencilTab &tab, const double *xs,
 #pragma unroll
                     for (int q = 0; q < Q; ++q) {
                         A.ym[d][q] = fma(c.x, yin[a][b][q], A.ym[d][q]);
-                        A.yk[d][q] = fma(c.y, yin[a][b][q], A.yk[d][q]);
+                        if (MK) A.yk[d][q] = fma(c.y, yin[a][b][q], A.yk[d][q]);
                     }
                 }
             }
 #pragma unroll
             for (int e = 0; e < 2; ++e) {                       // Z rows: o = (a-1, b-1, 1-e)
+                if (!MK) break;
                 const double c = st_coef<FAST>(tab, 2, clsZ, st_slot(2, 1, a - 1, b - 1, 1 - e)).y;
 #pragma unroll
                 for (int q = 0; q < Q; ++q) A.zk[e][q] = fma(c, yin[a][b][q], A.zk[e][q]);
@@ -166,12 +170,12 @@ __device__ __forceinline__ void st_push(const StencilTab &tab, const double *xs,
 #pragma unroll
                 for (int d = 1; d < 3; ++d) {                   // X, Y rows at s, s+1: o2 = 1 - d
                     const int o2 = 1 - d;
-                    if (a >= 1) {
+                    if (MK && a >= 1) {
                         const double c = st_coef<FAST>(tab, 0, clsX[d], st_slot(0, 2, a - 1, b - 1, o2)).y;
 #pragma unroll
                         for (int q = 0; q < Q; ++q) A.xk[d][q] = fma(c, zin[a][b][q], A.xk[d][q]);
                     }
-                    if (b >= 1) {
+                    if (MK && b >= 1) {
                         const double c = st_coef<FAST>(tab, 1, clsY[d], st_slot(1, 2, a - 1, b - 1, o2)).y;
 #pragma unroll
                         for (int q = 0; q < Q; ++q) A.yk[d][q] = fma(c, zin[a][b][q], A.yk[d][q]);
@@ -181,7 +185,7 @@ __device__ __forceinline__ void st_push(const StencilTab &tab, const double *xs,
 #pragma unroll
                 for (int q = 0; q < Q; ++q) {
                     A.zm[1][q] = fma(c.x, zin[a][b][q], A.zm[1][q]);
-                    A.zk[1][q] = fma(c.y, zin[a][b][q], A.zk[1][q]);
+                    if (MK) A.zk[1][q] = fma(c.y, zin[a][b][q], A.zk[1][q]);
                 }
             }
     }
@@ -371,7 +375,7 @@ __device__ __forceinline__ void st_time(const KT &kt, const StLane<Q> &L, const 
 // pre(T, row, own) (own-row values of the rows completing at this step; own = the staged block of
 // the row at its level) and emit<FAST>(T, row, cls, m[Q], k[Q]); every warp reaches every
 // barrier (also warps whose pencil lies outside the mesh).
-template <int Q, class Tl, bool LAST_REFILL, class Op>
+template <int Q, class Tl, bool LAST_REFILL, class Op, bool MK = true>
 __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, const StMaps &maps, StSmem<Q, Tl> &sm,
                                          int tile, int chunk, Op &op) {
     using C = StCfg<Q, Tl>;
@@ -422,7 +426,7 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
             const bool zin_ok = s < g.nz;
             if (fast) {
                 const int dummy[3] = {0, 0, 0};
-                st_push<Q, Tl, true, true>(tab, bb + ox, bb + oy, bb + oz, dummy, dummy, clsZ, A);
+                st_push<Q, Tl, true, true, MK>(tab, bb + ox, bb + oy, bb + oz, dummy, dummy, clsZ, A);
             } else {
                 int clsX[3], clsY[3];
 #pragma unroll
@@ -432,9 +436,9 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
                     clsY[d] = 3 * ci + cl;
                 }
                 if (zin_ok) {
-                    st_push<Q, Tl, false, true>(tab, bb + ox, bb + oy, bb + oz, clsX, clsY, clsZ, A);
+                    st_push<Q, Tl, false, true, MK>(tab, bb + ox, bb + oy, bb + oz, clsX, clsY, clsZ, A);
                 } else {
-                    st_push<Q, Tl, false, false>(tab, bb + ox, bb + oy, bb + oz, clsX, clsY, clsZ, A);
+                    st_push<Q, Tl, false, false, MK>(tab, bb + ox, bb + oy, bb + oz, clsX, clsY, clsZ, A);
                 }
             }
         }
@@ -639,6 +643,57 @@ k_st_sweep(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constan
                                  reinterpret_cast<char *>(out) + lane_off, rowbytes, (size_t)g.S * 8, omega_s, omega,
                                  bsl, {}, {}, {}};
     st_march<Q, Tl, true>(g, tab, maps, sm, tile, chunk, op);
+}
+
+// Mass form of the nodal residual's edge pass (Eq. (5); R17):
+// u = f - (Ct (x) M) x + (Nt (x) M) x_{k-1}, so that G^T u = G^T (f - L x) because K G = 0 (the
+// curl-curl part of L x lies in the kernel of G^T).  The march with the curl-curl FMAs compiled out:
+// 15 of the 21 inputs and ~60 of the ~290 FMAs per node-level.
+template <int Q>
+struct StResMassOp {
+    const KT &kt;
+    const char *fb;
+    char *ub;
+    unsigned rowbytes;
+    size_t bstride;
+    bool first;
+    const double *cpl;
+    double fv[3][Q], cv[3];
+    __device__ __forceinline__ void pre(int T, unsigned row, const double *) {
+        const char *p = fb + (size_t)row * rowbytes;
+#pragma unroll
+        for (int b = 0; b < Q; ++b) fv[T][b] = __ldg(reinterpret_cast<const double *>(p + b * bstride));
+        cv[T] = first && cpl ? __ldg(cpl + row) : 0.0;
+    }
+    template <bool FAST>
+    __device__ __forceinline__ void emit(int T, unsigned row, int, const double (&m)[Q], const double (&)[Q]) {
+        const double up = __shfl_up_sync(0xffffffffu, m[Q - 1], 1);
+        const double mp = first ? cv[T] : up;
+        const size_t off = (size_t)row * rowbytes;
+#pragma unroll
+        for (int b = 0; b < Q; ++b) {
+            double acc = fv[T][b] + (b == 0 ? mp : 0.0);
+#pragma unroll
+            for (int a = 0; a < Q; ++a) acc = fma(-kt.Ct[b * Q + a], m[a], acc);
+            *reinterpret_cast<double *>(ub + off + b * bstride) = acc;
+        }
+    }
+};
+
+template <int Q, class Tl = StTileRes>
+__global__ void __launch_bounds__(32 * Tl::Warps, 1)
+k_st_res_mass(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constant__ StMaps maps,
+              const double *__restrict__ cpl, const double *__restrict__ f, double *__restrict__ u, KT kt) {
+    extern __shared__ __align__(128) unsigned char st_dyn[];
+    StSmem<Q, Tl> &sm = *reinterpret_cast<StSmem<Q, Tl> *>(st_dyn + ((128u - (st_smem_addr(st_dyn) & 127u)) & 127u));
+    const int chunk = blockIdx.x / g.n_tiles, tile = blockIdx.x - chunk * g.n_tiles;
+    const unsigned rowbytes = (unsigned)(8u * Q * g.S);
+    const size_t lane_off = ((size_t)chunk * kStSPW + (threadIdx.x & 31)) * 8;
+    StResMassOp<Q> op{kt, reinterpret_cast<const char *>(f) + lane_off, reinterpret_cast<char *>(u) + lane_off,
+                      rowbytes, (size_t)g.S * 8, (threadIdx.x & 31) == 0,
+                      cpl ? cpl + (size_t)chunk * (g.Ex + g.Ey + (size_t)(g.nx + 1) * (g.ny + 1) * g.nz) : nullptr,
+                      {}, {}};
+    st_march<Q, Tl, false, StResMassOp<Q>, false>(g, tab, maps, sm, tile, chunk, op);
 }
 
 // The upwind coupling of each chunk's first slab (N_t = e_0 e_q^T): (M x_q) of the
