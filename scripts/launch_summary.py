@@ -35,8 +35,12 @@ def main(csv_path, bench_log, steps):
     print("total %.1f ms = %.1f ms / V-cycle serialised; bench.py (CUDA events, same command without ncu): %.1f ms / V-cycle"
           % (tot, tot / steps, d["ms_per_step"]))
     ev = sum(v["ms"] for v in d["kernels"].values())
-    tags = {"residual": ("k_residual", "k_st_residual"), "sweep_update": ("k_sweep", "k_st_sweep"),
-            "gtr_mass": ("k_res_mass",), "node_scan": ("k_node_scan",), "gt": ("k_gt<",),
+    # launch_res_mass / launch_residual run their chunk-coupling pre-passes inside the family's events
+    # (k_st_bslab, k_st_coupling: counted with the residual here, where most of them run)
+    tags = {"residual": ("k_residual", "k_st_residual", "k_st_bslab", "k_st_coupling"),
+            "sweep_update": ("k_sweep", "k_st_sweep"),
+            "gtr_mass": ("k_res_mass", "k_st_res_mass", "k_gtr"), "node_scan": ("k_node_scan", "k_sn_scan", "k_sn_carry"),
+            "gt": ("k_gt<",),
             "g_update": ("k_g_update",), "prolong": ("k_prolong",), "restrict": ("k_restrict",)}
     print("family shares, ncu / live events: " + ", ".join(
         "%s %.1f%% / %.1f%%" % (f, 100 * sum(v[1] for k, v in agg.items() if any(x in k for x in t)) / tot,
