@@ -40,8 +40,7 @@ static const char *const kVariantNames[] = {
     "sweep/chunked", "res_mass/spl1", "res_mass/spl2", "res_mass/spl4", "res_mass/chunked",
     "gtr/fused", "gtr/chunked", "gt/two-pass", "node_scan/multichunk", "node_scan/carry-in",
     "march/residual", "march/sweep", "restrict/space", "prolong/space", "stencil/residual",
-    "stencil/sweep", "stencil/res_mass", "coupling/prev", "stencil/node_scan", "coupling/side-output",
-    "stencil/split"};
+    "stencil/sweep", "stencil/res_mass", "coupling/prev", "stencil/node_scan", "coupling/side-output"};
 constexpr int kNumVariants = (int)(sizeof(kVariantNames) / sizeof(kVariantNames[0]));
 static std::atomic<unsigned long long> g_variants{0};
 static inline void note(int bit) { g_variants.fetch_or(1ull << bit, std::memory_order_relaxed); }
@@ -50,7 +49,7 @@ enum VariantBit {
     V_SWEEP_SPL1, V_SWEEP_SPL2, V_SWEEP_SPL4, V_SWEEP_CHUNKED, V_RM_SPL1, V_RM_SPL2, V_RM_SPL4, V_RM_CHUNKED,
     V_GTR_FUSED, V_GTR_CHUNKED, V_GT_TWOPASS, V_SCAN_MULTI, V_SCAN_CARRY, V_MARCH_RES, V_MARCH_SWEEP,
     V_RESTRICT_SPACE, V_PROLONG_SPACE, V_STENCIL_RES, V_STENCIL_SWEEP, V_STENCIL_RM, V_COUPLING_PREV,
-    V_SN_SCAN, V_BSLAB_SIDE, V_STENCIL_SPLIT
+    V_SN_SCAN, V_BSLAB_SIDE
 };
 unsigned long long variants(bool reset) {
     return reset ? g_variants.exchange(0) : g_variants.load();
@@ -65,9 +64,6 @@ KT make_kt(const TimeMats &tm) {
 }
 
 constexpr int kBlock = 256;
-#ifndef ST_SPLIT_DEFAULT
-#define ST_SPLIT_DEFAULT 7
-#endif
 
 // ---------------------------------------------------------------- helpers
 // y = D^{-1} v for the (Q x Q) Jacobi block D = Ct*dm + t*Mt*dk (cofactor inverse)
@@ -1318,13 +1314,6 @@ bool stencil_applies(const DevLevel &L, int Q) {
     return L.use_stencil && L.st_tab && (Q == 1 || Q == 2) && L.S % kStSPW == 0;
 }
 
-// Split march for dG(1) (lane = (time node, slab), 2 x Tl::Warps warps per CTA; stencil.cuh):
-// bit 0 residual, bit 1 sweep, bit 2 mass residual; env ST_SPLIT (tuning / A-B knob)
-static int stencil_split() {
-    const char *e = std::getenv("ST_SPLIT");        // read per launch: the parity tests switch it in-process
-    return e ? std::atoi(e) : ST_SPLIT_DEFAULT;
-}
-
 bool bslab_producer(const DevLevel &L, int Q) { return stencil_applies(L, Q) && L.st_bslab; }
 
 
@@ -1457,23 +1446,7 @@ int launch_residual(Stream st, const DevLevel &L, const KT &kt, int Q, const dou
                 stencil_smem_attr(kern, (int)sm);
                 kern<<<nb, nt, sm, st>>>(g, *L.st_tab, maps, cpl, L.tau, f, r, z, omega_s, kt, partial);
             };
-            if (QQ == 2 && (stencil_split() & 1)) {
-                note(V_STENCIL_SPLIT);
-                auto launch2 = [&](auto kern) {
-                    stencil_smem_attr(kern, (int)sm);
-                    kern<<<nb, 2 * nt, sm, st>>>(g, *L.st_tab, maps, cpl, L.tau, f, r, z, omega_s, kt, partial);
-                };
-                if (partial) {
-                    if (r) launch2(k_st_residual_s<true, false, true>);
-                    else launch2(k_st_residual_s<false, false, true>);
-                } else if (r && z) {
-                    launch2(k_st_residual_s<true, true, false>);
-                } else if (z) {
-                    launch2(k_st_residual_s<false, true, false>);
-                } else {
-                    launch2(k_st_residual_s<true, false, false>);
-                }
-            } else if (partial) {
+            if (partial) {
                 if (r) launch(k_st_residual<QQ, true, false, true>);
                 else launch(k_st_residual<QQ, false, false, true>);
             } else if (r && z) {
@@ -1549,18 +1522,7 @@ void launch_sweep(Stream st, const DevLevel &L, const KT &kt, int Q, bool last, 
                 kern<<<nb, nt, sm, st>>>(g, *L.st_tab, maps, L.tau, r, out, omega_s, omega, kt,
                                          last ? L.st_bslab : nullptr);
             };
-            if (QQ == 2 && (stencil_split() & 2)) {
-                note(V_STENCIL_SPLIT);
-                auto launch2 = [&](auto kern) {
-                    stencil_smem_attr(kern, (int)sm);
-                    kern<<<nb, 2 * nt, sm, st>>>(g, *L.st_tab, maps, L.tau, r, out, omega_s, omega, kt,
-                                                 last ? L.st_bslab : nullptr);
-                };
-                if (last && recon) launch2(k_st_sweep_s<true, true>);
-                else if (last) launch2(k_st_sweep_s<true, false>);
-                else if (recon) launch2(k_st_sweep_s<false, true>);
-                else launch2(k_st_sweep_s<false, false>);
-            } else if (last && recon) launch(k_st_sweep<QQ, true, true>);
+            if (last && recon) launch(k_st_sweep<QQ, true, true>);
             else if (last) launch(k_st_sweep<QQ, true, false>);
             else if (recon) launch(k_st_sweep<QQ, false, true>);
             else launch(k_st_sweep<QQ, false, false>);
@@ -1636,21 +1598,15 @@ void launch_res_mass(Stream st, const DevLevel &L, const KT &kt, int Q, const do
     if (stencil_applies(L, Q)) {
         note(V_STENCIL_RM);
         if (prev) note(V_COUPLING_PREV);
-        using Tl = StTileRes;
+        using Tl = StTileMass;
         const StGeo g = stencil_geo<Tl>(L);
         const size_t sm = Q == 1 ? sizeof(StSmem<1, Tl>) + 128 : sizeof(StSmem<2, Tl>) + 128;
         ST_DISPATCH_Q12(Q, {
             const double *cpl = stencil_coupling<QQ>(st, L, g, x, prev);
             StMaps maps;
             stencil_maps<QQ, Tl>(L, x, maps);
-            if (QQ == 2 && (stencil_split() & 4)) {
-                note(V_STENCIL_SPLIT);
-                stencil_smem_attr(k_st_res_mass_s<>, (int)sm);
-                k_st_res_mass_s<><<<grid(g), 64 * Tl::Warps, sm, st>>>(g, *L.st_tab, maps, cpl, L.tau, f, u, kt);
-            } else {
-                stencil_smem_attr(k_st_res_mass<QQ>, (int)sm);
-                k_st_res_mass<QQ><<<grid(g), 32 * Tl::Warps, sm, st>>>(g, *L.st_tab, maps, cpl, f, u, kt);
-            }
+            stencil_smem_attr(k_st_res_mass<QQ>, (int)sm);
+            k_st_res_mass<QQ><<<grid(g), 32 * Tl::Warps, sm, st>>>(g, *L.st_tab, maps, cpl, f, u, kt);
         });
         return;
     }

@@ -40,8 +40,19 @@ struct StTile {
 };
 // 4 x 3 pencils = 12 warps at <= 168 registers (sweep: measured 29.6 vs 34.0 ms per c4 V-cycle
 // for 4 x 2 pencils = 8 warps at 224 registers; 4 x 4 spills)
-using StTileRes = StTile<4, 3>;
-using StTileSweep = StTile<4, 3>;
+#ifndef ST_TILE_I
+#define ST_TILE_I 4
+#define ST_TILE_J 3
+#endif
+using StTileRes = StTile<ST_TILE_I, ST_TILE_J>;
+using StTileSweep = StTile<ST_TILE_I, ST_TILE_J>;
+// the mass-only march (k_st_res_mass) carries half the accumulators and is latency-bound: 20 warps at 96
+// registers (measured per c4 V-cycle: 9.37 ms at 4 x 3, 8.52 at 4 x 4, 7.75 at 5 x 4, 8.90 at 6 x 4)
+#ifndef ST_MTILE_I
+#define ST_MTILE_I 5
+#define ST_MTILE_J 4
+#endif
+using StTileMass = StTile<ST_MTILE_I, ST_MTILE_J>;
 constexpr int kStSPW = 32;                     // slabs per warp (lane = slab)
 constexpr int kStInterior = 4;                 // class (1, 1): both transverse coordinates inside
 
@@ -67,31 +78,43 @@ struct StAcc {
 // compiler-only barrier: keeps the shared-memory reads of the next input group after the FMAs of
 // this one, so that only one group of operands is live at a time (register budget -> warps/SM)
 __device__ __forceinline__ void st_phase() {
-    if (ST_PHASES) asm volatile("" ::: "memory");
+#if ST_PHASES
+    asm volatile("" ::: "memory");
+#endif
 }
 
 // xs / ys / zs: the warp's x-, y-, z-edge input blocks of the staged level, element (a, b, q) at
 // [(b * row + a) * Blk + q * 32] with row = the tile-box i extent of the edge type
 // MK = false: mass part only (the nodal residual's mass form, k_st_res_mass); the curl-curl FMAs and
 // the inputs only they read are compiled out
-// BQ: time nodes of a staged block (its stride); Q: time nodes this lane carries (Q = BQ, or 1 in
-// the split march below, where the lane's time node is part of its block offset)
-template <int Q, class Tl, bool FAST, bool ZIN, bool MK = true, int BQ = Q>
+template <int Q, class Tl, bool FAST, bool ZIN, bool MK = true>
 __device__ __forceinline__ void st_push(const StencilTab &tab, const double *xs, const double *ys, const double *zs,
                                         const int (&clsX)[3], const int (&clsY)[3], int clsZ, StAcc<Q> &A) {
-    constexpr int Blk = BQ * kStSPW;
+    constexpr int Blk = Q * kStSPW;
     double xin[2][3][Q], yin[3][2][Q], zin[3][3][Q];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
+    // input groups (one index a of an edge type): loads ...
+    auto ldx = [&](int a) {
 #pragma unroll
         for (int b = 0; b < 3; ++b)
 #pragma unroll
             for (int q = 0; q < Q; ++q) xin[a][b][q] = xs[(b * (Tl::TI + 1) + a) * Blk + q * kStSPW];
-    // loop order: input outermost, then the open levels d and time nodes q innermost, so that
-    // consecutive FMAs go to independent accumulators (latency of the fp64 pipe)
-    // ---- x-edge inputs xin[a][b] = x-edge (i-1+a, j-1+b)
+    };
+    auto ldy = [&](int a) {
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int q = 0; q < Q; ++q) yin[a][b][q] = ys[(b * (Tl::TI + 2) + a) * Blk + q * kStSPW];
+    };
+    auto ldz = [&](int a) {
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+            for (int q = 0; q < Q; ++q) zin[a][b][q] = zs[(b * (Tl::TI + 2) + a) * Blk + q * kStSPW];
+    };
+    // ... and FMAs.  Loop order: input outermost, then the open levels d and time nodes q innermost,
+    // so that consecutive FMAs go to independent accumulators (latency of the fp64 pipe)
+    // ---- x-edge inputs xin[a][b] = x-edge (i-1+a, j-1+b)
+    auto fx = [&](int a) {
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
 #pragma unroll
@@ -119,16 +142,9 @@ __device__ __forceinline__ void st_push(const StencilTab &tab, const double *xs,
                 for (int q = 0; q < Q; ++q) A.zk[e][q] = fma(c, xin[a][b][q], A.zk[e][q]);
             }
         }
+    };
     // ---- y-edge inputs yin[a][b] = y-edge (i-1+a, j-1+b)
-    st_phase();
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b)
-#pragma unroll
-            for (int q = 0; q < Q; ++q) yin[a][b][q] = ys[(b * (Tl::TI + 2) + a) * Blk + q * kStSPW];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
+    auto fy = [&](int a) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
 #pragma unroll
@@ -156,41 +172,76 @@ __device__ __forceinline__ void st_push(const StencilTab &tab, const double *xs,
                 for (int q = 0; q < Q; ++q) A.zk[e][q] = fma(c, yin[a][b][q], A.zk[e][q]);
             }
         }
+    };
     // ---- z-edge inputs zin[a][b] = z-edge (i-1+a, j-1+b) from level s to s+1
-    if (ZIN) {
-        st_phase();
+    auto fz = [&](int a) {
 #pragma unroll
-        for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
 #pragma unroll
-            for (int b = 0; b < 3; ++b)
+            for (int d = 1; d < 3; ++d) {                       // X, Y rows at s, s+1: o2 = 1 - d
+                const int o2 = 1 - d;
+                if (MK && a >= 1) {
+                    const double c = st_coef<FAST>(tab, 0, clsX[d], st_slot(0, 2, a - 1, b - 1, o2)).y;
 #pragma unroll
-                for (int q = 0; q < Q; ++q) zin[a][b][q] = zs[(b * (Tl::TI + 2) + a) * Blk + q * kStSPW];
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-#pragma unroll
-                for (int d = 1; d < 3; ++d) {                   // X, Y rows at s, s+1: o2 = 1 - d
-                    const int o2 = 1 - d;
-                    if (MK && a >= 1) {
-                        const double c = st_coef<FAST>(tab, 0, clsX[d], st_slot(0, 2, a - 1, b - 1, o2)).y;
-#pragma unroll
-                        for (int q = 0; q < Q; ++q) A.xk[d][q] = fma(c, zin[a][b][q], A.xk[d][q]);
-                    }
-                    if (MK && b >= 1) {
-                        const double c = st_coef<FAST>(tab, 1, clsY[d], st_slot(1, 2, a - 1, b - 1, o2)).y;
-#pragma unroll
-                        for (int q = 0; q < Q; ++q) A.yk[d][q] = fma(c, zin[a][b][q], A.yk[d][q]);
-                    }
+                    for (int q = 0; q < Q; ++q) A.xk[d][q] = fma(c, zin[a][b][q], A.xk[d][q]);
                 }
-                const double2 c = st_coef<FAST>(tab, 2, clsZ, st_slot(2, 2, a - 1, b - 1, 0));   // Z row at s
+                if (MK && b >= 1) {
+                    const double c = st_coef<FAST>(tab, 1, clsY[d], st_slot(1, 2, a - 1, b - 1, o2)).y;
 #pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    A.zm[1][q] = fma(c.x, zin[a][b][q], A.zm[1][q]);
-                    if (MK) A.zk[1][q] = fma(c.y, zin[a][b][q], A.zk[1][q]);
+                    for (int q = 0; q < Q; ++q) A.yk[d][q] = fma(c, zin[a][b][q], A.yk[d][q]);
                 }
             }
+            const double2 c = st_coef<FAST>(tab, 2, clsZ, st_slot(2, 2, a - 1, b - 1, 0));   // Z row at s
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                A.zm[1][q] = fma(c.x, zin[a][b][q], A.zm[1][q]);
+                if (MK) A.zk[1][q] = fma(c.y, zin[a][b][q], A.zk[1][q]);
+            }
+        }
+    };
+#if ST_PHASES == 2
+    // one group ahead: the shared-memory reads of group g + 1 are issued before the FMAs of group g
+    // (at most two groups of <= 3 inputs live; the order of the FMAs on every accumulator is that
+    // of the three-phase form below)
+    ldx(0);
+    ldx(1); st_phase(); fx(0);
+    ldy(0); st_phase(); fx(1);
+    ldy(1); st_phase(); fy(0);
+    ldy(2); st_phase(); fy(1);
+    if (ZIN) ldz(0);
+    st_phase(); fy(2);
+    if (ZIN) {
+        ldz(1); st_phase(); fz(0);
+        ldz(2); st_phase(); fz(1);
+        st_phase(); fz(2);
     }
+#elif ST_PHASES == 3
+    // two groups ahead
+    ldx(0); ldx(1);
+    ldy(0); st_phase(); fx(0);
+    ldy(1); st_phase(); fx(1);
+    ldy(2); st_phase(); fy(0);
+    if (ZIN) ldz(0);
+    st_phase(); fy(1);
+    if (ZIN) ldz(1);
+    st_phase(); fy(2);
+    if (ZIN) {
+        ldz(2); st_phase(); fz(0);
+        st_phase(); fz(1);
+        st_phase(); fz(2);
+    }
+#else
+    ldx(0); ldx(1);
+    fx(0); fx(1);
+    st_phase();
+    ldy(0); ldy(1); ldy(2);
+    fy(0); fy(1); fy(2);
+    if (ZIN) {
+        st_phase();
+        ldz(0); ldz(1); ldz(2);
+        fz(0); fz(1); fz(2);
+    }
+#endif
 }
 
 // ------------------------------------------------------------- TMA staging
@@ -377,22 +428,11 @@ __device__ __forceinline__ void st_time(const KT &kt, const StLane<Q> &L, const 
 // pre(T, row, own) (own-row values of the rows completing at this step; own = the staged block of
 // the row at its level) and emit<FAST>(T, row, cls, m[Q], k[Q]); every warp reaches every
 // barrier (also warps whose pencil lies outside the mesh).
-// SPLIT (Q = 2): the CTA has 2 x Tl::Warps warps; warp w and warp w + Tl::Warps share pencil w, each
-// taking 16 of the chunk's 32 slabs with lane = (time node, slab): lanes 0-15 time node 0, lanes
-// 16-31 time node 1.  Every lane then carries ONE time node: half the accumulators and inputs per
-// thread, twice the resident warps ("split march").  Op works on m[1], k[1] and
-// exchanges time nodes by shuffles; op.xchg passes the mass accumulators of slab 15 to the warp
-// of slabs 16-31 for the upwind coupling of slab 16.
-template <int Q, class Tl, bool LAST_REFILL, class Op, bool MK = true, bool SPLIT = false>
+template <int Q, class Tl, bool LAST_REFILL, class Op, bool MK = true>
 __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, const StMaps &maps, StSmem<Q, Tl> &sm,
                                          int tile, int chunk, Op &op) {
     using C = StCfg<Q, Tl>;
-    static_assert(!SPLIT || Q == 2, "split march: dG(1) only");
-    constexpr int QL = SPLIT ? 1 : Q;           // time nodes per lane
-    const int warp = SPLIT ? (int)(threadIdx.x >> 5) % Tl::Warps : (int)(threadIdx.x >> 5);
-    const int l32 = threadIdx.x & 31;
-    // offset of the lane's first value inside a staged block ([time node][slab])
-    const int lane = SPLIT ? (l32 >> 4) * kStSPW + ((int)(threadIdx.x >> 5) / Tl::Warps) * 16 + (l32 & 15) : l32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ti = tile % g.tiles_i, tj = tile / g.tiles_i;
     const int i0 = ti * Tl::TI, j0 = tj * Tl::TJ;
     const int wi = warp % Tl::TI, wj = warp / Tl::TI;
@@ -407,13 +447,13 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
     __syncthreads();
     if (threadIdx.x == 0)
         for (int s = 0; s < kStNB && s <= g.nz; ++s) st_stage<Q, Tl>(g, maps, sm, s, i0, j0, k0);
-    StAcc<QL> A;
+    StAcc<Q> A;
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
-        for (int q = 0; q < QL; ++q) A.xm[d][q] = A.xk[d][q] = A.ym[d][q] = A.yk[d][q] = 0.0;
+        for (int q = 0; q < Q; ++q) A.xm[d][q] = A.xk[d][q] = A.ym[d][q] = A.yk[d][q] = 0.0;
 #pragma unroll
-    for (int q = 0; q < QL; ++q) A.zm[0][q] = A.zk[0][q] = A.zm[1][q] = A.zk[1][q] = 0.0;
+    for (int q = 0; q < Q; ++q) A.zm[0][q] = A.zk[0][q] = A.zm[1][q] = A.zk[1][q] = 0.0;
     const int ci = st_cls(i, g.nx), cj = st_cls(j, g.ny);
     const bool inner_pencil = ci == 1 && cj == 1;
     const int clsZ = 3 * ci + cj;
@@ -439,7 +479,7 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
             const bool zin_ok = s < g.nz;
             if (fast) {
                 const int dummy[3] = {0, 0, 0};
-                st_push<QL, Tl, true, true, MK, Q>(tab, bb + ox, bb + oy, bb + oz, dummy, dummy, clsZ, A);
+                st_push<Q, Tl, true, true, MK>(tab, bb + ox, bb + oy, bb + oz, dummy, dummy, clsZ, A);
             } else {
                 int clsX[3], clsY[3];
 #pragma unroll
@@ -449,14 +489,13 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
                     clsY[d] = 3 * ci + cl;
                 }
                 if (zin_ok) {
-                    st_push<QL, Tl, false, true, MK, Q>(tab, bb + ox, bb + oy, bb + oz, clsX, clsY, clsZ, A);
+                    st_push<Q, Tl, false, true, MK>(tab, bb + ox, bb + oy, bb + oz, clsX, clsY, clsZ, A);
                 } else {
-                    st_push<QL, Tl, false, false, MK, Q>(tab, bb + ox, bb + oy, bb + oz, clsX, clsY, clsZ, A);
+                    st_push<Q, Tl, false, false, MK>(tab, bb + ox, bb + oy, bb + oz, clsX, clsY, clsZ, A);
                 }
             }
         }
         if (s >= 1) {
-            if constexpr (SPLIT) op.xchg(A.xm[0][0], A.ym[0][0], A.zm[0][0]);
             const int cl = st_cls(l, g.nz);
             if (fast) {
                 if (eX) op.template emit<true>(0, rX, kStInterior, A.xm[0], A.xk[0]);
@@ -469,7 +508,7 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
             }
         }
 #pragma unroll
-        for (int q = 0; q < QL; ++q) {
+        for (int q = 0; q < Q; ++q) {
             A.xm[0][q] = A.xm[1][q]; A.xm[1][q] = A.xm[2][q]; A.xm[2][q] = 0.0;
             A.xk[0][q] = A.xk[1][q]; A.xk[1][q] = A.xk[2][q]; A.xk[2][q] = 0.0;
             A.ym[0][q] = A.ym[1][q]; A.ym[1][q] = A.ym[2][q]; A.ym[2][q] = 0.0;
@@ -480,7 +519,7 @@ __device__ __forceinline__ void st_march(const StGeo &g, const StencilTab &tab, 
         // this warp is done with level s-1 (own values): once every warp is, refill its buffer
         // with level s-1+kStNB
         if (LAST_REFILL) {
-            if (s >= 1 && s - 1 + kStNB <= g.nz && st_release<(SPLIT ? 2 : 1) * Tl::Warps>(&sm.done[(s - 1) % kStNB]) &&
+            if (s >= 1 && s - 1 + kStNB <= g.nz && st_release<Tl::Warps>(&sm.done[(s - 1) % kStNB]) &&
                 (threadIdx.x & 31) == 0)
                 st_stage<Q, Tl>(g, maps, sm, s - 1 + kStNB, i0, j0, k0);
         } else {
@@ -694,7 +733,7 @@ struct StResMassOp {
     }
 };
 
-template <int Q, class Tl = StTileRes>
+template <int Q, class Tl = StTileMass>
 __global__ void __launch_bounds__(32 * Tl::Warps, 1)
 k_st_res_mass(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constant__ StMaps maps,
               const double *__restrict__ cpl, const double *__restrict__ f, double *__restrict__ u, KT kt) {
@@ -708,288 +747,6 @@ k_st_res_mass(StGeo g, const __grid_constant__ StencilTab tab, const __grid_cons
                       cpl ? cpl + (size_t)chunk * (g.Ex + g.Ey + (size_t)(g.nx + 1) * (g.ny + 1) * g.nz) : nullptr,
                       {}, {}};
     st_march<Q, Tl, false, StResMassOp<Q>, false>(g, tab, maps, sm, tile, chunk, op);
-}
-
-// ------------------------------------------------------------------ split march (dG(1))
-// lane = (time node b, slab): the same kernels with every lane carrying one time node of one slab
-// (st_march<SPLIT>).  The (2 x 2) time blocks of R1 are applied with the partner lane's values
-// (lane ^ 16, one shuffle per operand) in the order of st_time / the unsplit epilogues, so the
-// results are bitwise those of the unsplit kernels.
-struct StLaneS {
-    int k, sl, b, half;             // slab, slab in the chunk, time node, which 16 slabs of the chunk
-    double t;                       // tau_k
-    double ct[2], tm[2];            // row b of Ct and of tau_k Mt
-};
-
-__device__ __forceinline__ void st_lane_s(const KT &kt, const double *__restrict__ tau, int chunk, int n_pencils,
-                                          StLaneS &L) {
-    const int l32 = threadIdx.x & 31;
-    L.half = (int)(threadIdx.x >> 5) / n_pencils;
-    L.b = l32 >> 4;
-    L.sl = L.half * 16 + (l32 & 15);
-    L.k = chunk * kStSPW + L.sl;
-    L.t = __ldg(tau + L.k);
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-        L.ct[a] = L.b ? kt.Ct[2 + a] : kt.Ct[a];
-        L.tm[a] = L.t * (L.b ? kt.Mt[2 + a] : kt.Mt[a]);
-    }
-}
-
-// interior-class block table of the chunk's 32 slabs, built by threads 0..31 (thread = slab)
-__device__ __forceinline__ void st_block_table_s(const StencilTab &tab, const KT &kt, const double *__restrict__ tau,
-                                                 int chunk, StBlockTab<2> &bt) {
-    if (threadIdx.x < 32) {
-        StLane<2> L0;
-        L0.k = chunk * kStSPW + threadIdx.x;
-        L0.t = __ldg(tau + L0.k);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) L0.tMt[i] = L0.t * kt.Mt[i];
-#pragma unroll
-        for (int T = 0; T < 3; ++T) {
-            const double2 dd = tab.c[T][kStInterior][st_slot(T, T, 0, 0, 0)];
-            double D[4], Di[4];
-            st_block<2>(kt, L0, dd.x, dd.y, D, Di);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { bt.v[T][i][threadIdx.x] = D[i]; bt.v[T][4 + i][threadIdx.x] = Di[i]; }
-        }
-    }
-}
-
-// own and partner value ordered by time node
-__device__ __forceinline__ void st_pair(const StLaneS &L, double v, double &v0, double &v1) {
-    const double o = __shfl_xor_sync(0xffffffffu, v, 16);
-    v0 = L.b ? o : v;
-    v1 = L.b ? v : o;
-}
-
-// (A x)_b of the lane's time node b (st_time's order of operations)
-__device__ __forceinline__ double st_time_s(const StLaneS &L, double m, double k) {
-    double m0, m1, k0, k1;
-    st_pair(L, m, m0, m1);
-    st_pair(L, k, k0, k1);
-    double acc = fma(L.ct[0], m0, fma(L.tm[0], k0, 0.0));
-    return fma(L.ct[1], m1, fma(L.tm[1], k1, acc));
-}
-
-// row b of D^{-1} of the row's class
-template <bool FAST>
-__device__ __forceinline__ void st_dinv_s(const StencilTab &tab, const KT &kt, const StLaneS &L,
-                                          const StBlockTab<2> &bt, int T, int cls, double &d0, double &d1) {
-    if (FAST) {
-        d0 = bt.v[T][4 + 2 * L.b][L.sl];
-        d1 = bt.v[T][5 + 2 * L.b][L.sl];
-    } else {
-        const double2 dd = st_coef<false>(tab, T, cls, st_slot(T, T, 0, 0, 0));
-        StLane<2> L0;
-        L0.k = L.k; L0.t = L.t;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) L0.tMt[i] = L.t * kt.Mt[i];
-        double D[4], Di[4];
-        st_block<2>(kt, L0, dd.x, dd.y, D, Di);
-        d0 = L.b ? Di[2] : Di[0];
-        d1 = L.b ? Di[3] : Di[1];
-    }
-}
-
-// Upwind coupling in the split layout: time node 0 of slab j takes (M x_1) of slab j - 1 from lane
-// 16 + j - 1 of its own warp; slab 0 of the chunk from k_st_coupling (cpl); slab 16 (first lane of
-// the second warp of the pencil) from lane 31 of the first warp, through shared memory and a
-// 64-thread named barrier of the pencil's two warps.
-struct StCplS {
-    bool first, mid, src;           // chunk's first slab (time node 0) / slab 16 (time node 0) / slab 15 (time node 1)
-    const double *cpl;
-    double *xch;                    // the pencil's 3 exchange slots
-    unsigned bar;                   // named barrier of the pencil's two warps
-    double cv[3];
-    __device__ __forceinline__ void init(const StLaneS &L, const double *cpl_, double *xch_, int pencil) {
-        const int l32 = threadIdx.x & 31;
-        first = L.half == 0 && l32 == 0;
-        mid = L.half == 1 && l32 == 0;
-        src = L.half == 0 && l32 == 31;
-        cpl = cpl_;
-        xch = xch_ + 3 * pencil;
-        bar = 1u + (unsigned)pencil;
-    }
-    __device__ __forceinline__ void pre(int T, unsigned row) { cv[T] = first && cpl ? __ldg(cpl + row) : 0.0; }
-    __device__ __forceinline__ void xchg(double mx, double my, double mz) {
-        if (src) { xch[0] = mx; xch[1] = my; xch[2] = mz; }
-        asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
-        if (mid) { cv[0] = xch[0]; cv[1] = xch[1]; cv[2] = xch[2]; }
-    }
-    // the coupling term of the lane's row (0 for time node 1)
-    __device__ __forceinline__ double term(const StLaneS &L, int T, double m) const {
-        const double up = __shfl_sync(0xffffffffu, m, ((threadIdx.x & 31) + 15) & 31);
-        const double mp = (first || mid) ? cv[T] : up;
-        return L.b == 0 ? mp : 0.0;
-    }
-};
-
-template <bool R_OUT, bool Z_OUT, bool NORM>
-struct StResOpS {
-    const StencilTab &tab;
-    const KT &kt;
-    const StLaneS &L;
-    const StBlockTab<2> &bt;
-    const char *fb;                 // f + (b S + k) elements, in bytes
-    char *rb, *zb;
-    unsigned rowbytes;
-    double omega_s;
-    StCplS c;
-    double nrm;
-    double fv[3];
-    __device__ __forceinline__ void pre(int T, unsigned row, const double *) {
-        fv[T] = __ldg(reinterpret_cast<const double *>(fb + (size_t)row * rowbytes));
-        c.pre(T, row);
-    }
-    __device__ __forceinline__ void xchg(double mx, double my, double mz) { c.xchg(mx, my, mz); }
-    template <bool FAST>
-    __device__ __forceinline__ void emit(int T, unsigned row, int cls, const double (&m)[1], const double (&k)[1]) {
-        const double ax = st_time_s(L, m[0], k[0]);
-        const double rr = fv[T] - ax + c.term(L, T, m[0]);
-        const size_t off = (size_t)row * rowbytes;
-        if (R_OUT) *reinterpret_cast<double *>(rb + off) = rr;
-        if (Z_OUT) {
-            double d0, d1, r0, r1;
-            st_dinv_s<FAST>(tab, kt, L, bt, T, cls, d0, d1);
-            st_pair(L, rr, r0, r1);
-            *reinterpret_cast<double *>(zb + off) = omega_s * fma(d1, r1, fma(d0, r0, 0.0));
-        }
-        if (NORM) nrm = fma(rr, rr, nrm);
-    }
-};
-
-template <bool R_OUT, bool Z_OUT, bool NORM, class Tl = StTileRes>
-__global__ void __launch_bounds__(64 * Tl::Warps, 1)
-k_st_residual_s(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constant__ StMaps maps,
-                const double *__restrict__ cpl, const double *__restrict__ tau, const double *__restrict__ f,
-                double *__restrict__ r, double *__restrict__ z, double omega_s, KT kt, double *__restrict__ partial) {
-    extern __shared__ __align__(128) unsigned char st_dyn[];
-    StSmem<2, Tl> &sm = *reinterpret_cast<StSmem<2, Tl> *>(st_dyn + ((128u - (st_smem_addr(st_dyn) & 127u)) & 127u));
-    __shared__ StBlockTab<2> bt;
-    __shared__ double xch[3 * Tl::Warps];
-    const int chunk = blockIdx.x / g.n_tiles, tile = blockIdx.x - chunk * g.n_tiles;
-    StLaneS L;
-    st_lane_s(kt, tau, chunk, Tl::Warps, L);
-    st_block_table_s(tab, kt, tau, chunk, bt);    // (the march's first barrier publishes it)
-    const unsigned rowbytes = (unsigned)(16u * g.S);
-    const size_t lane_off = ((size_t)L.b * g.S + L.k) * 8;
-    StResOpS<R_OUT, Z_OUT, NORM> op{tab, kt, L, bt, reinterpret_cast<const char *>(f) + lane_off,
-                                    reinterpret_cast<char *>(r) + lane_off, reinterpret_cast<char *>(z) + lane_off,
-                                    rowbytes, omega_s, {}, 0.0, {}};
-    op.c.init(L, cpl ? cpl + (size_t)chunk * (g.Ex + g.Ey + (size_t)(g.nx + 1) * (g.ny + 1) * g.nz) : nullptr, xch,
-              (int)(threadIdx.x >> 5) % Tl::Warps);
-    st_march<2, Tl, false, decltype(op), true, true>(g, tab, maps, sm, tile, chunk, op);
-    if (NORM) {
-        __shared__ double sh[2 * Tl::Warps];
-        const double s = block_reduce_sum(op.nrm, sh);
-        if (threadIdx.x == 0) partial[blockIdx.x] = s;
-    }
-}
-
-template <bool LAST, bool RECON>
-struct StSweepOpS {
-    const StencilTab &tab;
-    const KT &kt;
-    const StLaneS &L;
-    const StBlockTab<2> &bt;
-    const char *rb;
-    char *ob;
-    unsigned rowbytes;
-    double omega_s, omega;
-    double *bsl;                    // LAST: x_q of the chunk's last slab (time node 1, slab 31), or null
-    double zv[3], rv[3], xv[3];
-    __device__ __forceinline__ void pre(int T, unsigned row, const double *own) {
-        const size_t off = (size_t)row * rowbytes;
-        zv[T] = own[0];
-        if (!RECON) rv[T] = __ldg(reinterpret_cast<const double *>(rb + off));
-        if (LAST) xv[T] = *reinterpret_cast<const double *>(ob + off);
-    }
-    __device__ __forceinline__ void xchg(double, double, double) {}
-    template <bool FAST>
-    __device__ __forceinline__ void emit(int T, unsigned row, int cls, const double (&m)[1], const double (&k)[1]) {
-        const double az = st_time_s(L, m[0], k[0]);
-        const double d = RECON ? az : rv[T] - az;
-        double d0, d1, e0, e1;
-        st_dinv_s<FAST>(tab, kt, L, bt, T, cls, d0, d1);
-        st_pair(L, d, e0, e1);
-        const double y = fma(d1, e1, fma(d0, e0, 0.0));
-        const double res = RECON ? fma(-omega_s, y, 2.0 * zv[T]) : fma(omega_s, y, zv[T]);
-        double *o = reinterpret_cast<double *>(ob + (size_t)row * rowbytes);
-        if (LAST) {
-            const double xn = fma(omega, res, xv[T]);
-            *o = xn;
-            if (bsl) bsl[row] = xn;
-        } else {
-            *o = res;
-        }
-    }
-};
-
-template <bool LAST, bool RECON, class Tl = StTileSweep>
-__global__ void __launch_bounds__(64 * Tl::Warps, 1)
-k_st_sweep_s(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constant__ StMaps maps,
-             const double *__restrict__ tau, const double *__restrict__ r, double *out, double omega_s, double omega,
-             KT kt, double *__restrict__ bslab) {
-    extern __shared__ __align__(128) unsigned char st_dyn[];
-    StSmem<2, Tl> &sm = *reinterpret_cast<StSmem<2, Tl> *>(st_dyn + ((128u - (st_smem_addr(st_dyn) & 127u)) & 127u));
-    __shared__ StBlockTab<2> bt;
-    const int chunk = blockIdx.x / g.n_tiles, tile = blockIdx.x - chunk * g.n_tiles;
-    StLaneS L;
-    st_lane_s(kt, tau, chunk, Tl::Warps, L);
-    st_block_table_s(tab, kt, tau, chunk, bt);
-    const unsigned rowbytes = (unsigned)(16u * g.S);
-    const size_t lane_off = ((size_t)L.b * g.S + L.k) * 8;
-    const size_t n_edges = (size_t)g.Ex + g.Ey + (size_t)(g.nx + 1) * (g.ny + 1) * g.nz;
-    // the lane of (time node 1, slab 31) records x_q for the next chunk's coupling (k_st_bslab layout)
-    double *bsl = (LAST && bslab && L.b == 1 && L.sl == 31 && chunk + 1 < g.n_chunks)
-                      ? bslab + (size_t)(chunk + 1) * n_edges : nullptr;
-    StSweepOpS<LAST, RECON> op{tab, kt, L, bt, reinterpret_cast<const char *>(r) + lane_off,
-                               reinterpret_cast<char *>(out) + lane_off, rowbytes, omega_s, omega, bsl, {}, {}, {}};
-    st_march<2, Tl, true, decltype(op), true, true>(g, tab, maps, sm, tile, chunk, op);
-}
-
-struct StResMassOpS {
-    const StLaneS &L;
-    const char *fb;
-    char *ub;
-    unsigned rowbytes;
-    StCplS c;
-    double fv[3];
-    __device__ __forceinline__ void pre(int T, unsigned row, const double *) {
-        fv[T] = __ldg(reinterpret_cast<const double *>(fb + (size_t)row * rowbytes));
-        c.pre(T, row);
-    }
-    __device__ __forceinline__ void xchg(double mx, double my, double mz) { c.xchg(mx, my, mz); }
-    template <bool FAST>
-    __device__ __forceinline__ void emit(int T, unsigned row, int, const double (&m)[1], const double (&)[1]) {
-        double m0, m1;
-        st_pair(L, m[0], m0, m1);
-        double acc = fv[T] + c.term(L, T, m[0]);
-        acc = fma(-L.ct[0], m0, acc);
-        acc = fma(-L.ct[1], m1, acc);
-        *reinterpret_cast<double *>(ub + (size_t)row * rowbytes) = acc;
-    }
-};
-
-template <class Tl = StTileRes>
-__global__ void __launch_bounds__(64 * Tl::Warps, 1)
-k_st_res_mass_s(StGeo g, const __grid_constant__ StencilTab tab, const __grid_constant__ StMaps maps,
-                const double *__restrict__ cpl, const double *__restrict__ tau, const double *__restrict__ f,
-                double *__restrict__ u, KT kt) {
-    extern __shared__ __align__(128) unsigned char st_dyn[];
-    StSmem<2, Tl> &sm = *reinterpret_cast<StSmem<2, Tl> *>(st_dyn + ((128u - (st_smem_addr(st_dyn) & 127u)) & 127u));
-    __shared__ double xch[3 * Tl::Warps];
-    const int chunk = blockIdx.x / g.n_tiles, tile = blockIdx.x - chunk * g.n_tiles;
-    StLaneS L;
-    st_lane_s(kt, tau, chunk, Tl::Warps, L);
-    const unsigned rowbytes = (unsigned)(16u * g.S);
-    const size_t lane_off = ((size_t)L.b * g.S + L.k) * 8;
-    StResMassOpS op{L, reinterpret_cast<const char *>(f) + lane_off, reinterpret_cast<char *>(u) + lane_off, rowbytes,
-                    {}, {}};
-    op.c.init(L, cpl ? cpl + (size_t)chunk * (g.Ex + g.Ey + (size_t)(g.nx + 1) * (g.ny + 1) * g.nz) : nullptr, xch,
-              (int)(threadIdx.x >> 5) % Tl::Warps);
-    st_march<2, Tl, false, decltype(op), false, true>(g, tab, maps, sm, tile, chunk, op);
 }
 
 // The upwind coupling of each chunk's first slab (N_t = e_0 e_q^T): (M x_q) of the

@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_stencil.py -x -q -p no:cacheprovider > gpurun_out/s_t.log 2>&1; echo t=$?
-tail -15 gpurun_out/s_t.log
-for v in 7 0 3 7 0; do ST_SPLIT=$v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/s_b$v.json 2>>gpurun_out/s_b.err; python -c "
-import json;d=json.load(open('gpurun_out/s_b$v.json'));print('split=$v', round(d['ms_per_step'],2), {k:round(v['ms'],1) for k,v in d['kernels'].items()}, {k:round(v['GBps']) for k,v in d['kernels'].items()}, d['clocks']['sm_mhz'])"; done
-tail -5 gpurun_out/s_b.err
+for i in 1 2; do
+for l in paper_1911_09548_b200/libst.so variants_tmp/libst_m54.so variants_tmp/libst_m64.so; do
+  timeout 300 python scripts/variant_check.py $l 5 2>&1 | tail -1
+done; done | tee gpurun_out/v_mtiles.log
+timeout 600 python -m pytest tests/test_gpu_stencil.py tests/test_gpu_bench_paths.py -x -q -p no:cacheprovider 2>&1 | tail -3

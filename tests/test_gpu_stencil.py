@@ -125,40 +125,3 @@ def test_node_stencil_matches_ell(torch_cuda, monkeypatch):
         s.close()
     monkeypatch.delenv("ST_NODE_STENCIL")
     assert float(np.abs(outs[0] - outs[1]).max()) <= 1e-12 * float(np.abs(outs[1]).max())
-
-
-SPLIT_CASES = [((2, 3, 4), 64), ((5, 3, 3), 32), ((8, 8, 8), 96), ((9, 7, 5), 64)]
-
-
-@pytest.mark.parametrize("n,S", SPLIT_CASES, ids=[f"{c[0]}x{c[1]}" for c in SPLIT_CASES])
-def test_split_march_bitwise(torch_cuda, n, S, monkeypatch):
-    # dG(1): the split march (lane = (time node, slab), ST_SPLIT=7, the default) applies the same
-    # operations in the same order as the one-slab-per-lane march (ST_SPLIT=0): residual, the
-    # V-cycle (residual + first sweep, second sweep, mass residual) bitwise equal; the norm is
-    # reduced in another order.  Slab 16 of every chunk takes its upwind coupling from the
-    # pencil's other warp (several chunks, boundary classes, partial tiles covered by the cases).
-    import paper_1911_09548_b200 as p
-    torch = torch_cuda
-    w = uniform_case(n, S, 1)
-    rng = np.random.default_rng(31)
-    F = workloads.from_oracle(rng.uniform(-1, 1, (S, 2, w.n_edges)))
-    X0 = workloads.from_oracle(rng.uniform(-1, 1, (S, 2, w.n_edges)))
-    outs = []
-    for env in ("0", "7"):
-        monkeypatch.setenv("ST_SPLIT", env)
-        s = p.Solver.from_workload(w)
-        x = torch.from_numpy(X0).cuda()
-        f = torch.from_numpy(F).cuda()
-        r = torch.empty_like(f)
-        p.kernel_variants(reset=True)
-        s.residual(x, f, r)
-        rn, _ = s.residual(x, f, norms=True)
-        s.vcycle(x, f)
-        torch.cuda.synchronize()
-        assert ("stencil/split" in p.kernel_variants(reset=True)) == (env == "7")
-        outs.append((r.cpu().numpy(), rn, x.cpu().numpy()))
-        s.close()
-    monkeypatch.delenv("ST_SPLIT")
-    assert np.array_equal(outs[0][0], outs[1][0])
-    assert outs[0][1] == pytest.approx(outs[1][1], rel=1e-13)
-    assert np.array_equal(outs[0][2], outs[1][2])
