@@ -38,11 +38,14 @@ struct StTile {
     static constexpr int BY = (TI_ + 2) * (TJ_ + 1);
     static constexpr int BZ = (TI_ + 2) * (TJ_ + 2);
 };
-// 4 x 3 pencils = 12 warps at <= 168 registers (sweep: measured 29.6 vs 34.0 ms per c4 V-cycle
-// for 4 x 2 pencils = 8 warps at 224 registers; 4 x 4 spills)
+// 12 warps at <= 168 registers (3 warps per scheduler; 13-16 warps would cap at 128 registers).
+// Measured per c4 V-cycle (65 x 65 pencils per level-0 z-plane), residual / sweep family: 4 x 2 pencils
+// (8 warps, 224 registers) 34.0 ms sweep; 4 x 3: 32.1 / 25.3; 3 x 4: 32.0 / 25.2; 6 x 2: 31.3 / 24.7
+// (66 x 66 covered instead of 68 x 66); 4 x 4 (16 warps, 128 registers, 4-140 B spills): 33.6 / 26.8;
+// 7 x 2 (14 warps, 128 registers): 35.8 / 29.9
 #ifndef ST_TILE_I
-#define ST_TILE_I 4
-#define ST_TILE_J 3
+#define ST_TILE_I 6
+#define ST_TILE_J 2
 #endif
 using StTileRes = StTile<ST_TILE_I, ST_TILE_J>;
 using StTileSweep = StTile<ST_TILE_I, ST_TILE_J>;
