@@ -134,9 +134,9 @@ def ncu_traffic(family):
     return None, "family not in the capture"
 
 
-def link_bandwidth(torch, host, dev, stream):
+def link_bandwidth(torch, host, dev, stream, host2=None, dev2=None):
     """Pinned host <-> device copy bandwidth of this box per direction (GB/s), the bound of the
-    e2e number: one full-vector copy each way, CUDA events."""
+    e2e number: one full-vector copy each way alone, then both directions at once; CUDA events."""
     out = {}
     with torch.cuda.stream(stream):
         for name, dst, src in (("h2d", dev, host), ("d2h", host, dev)):
@@ -147,6 +147,25 @@ def link_bandwidth(torch, host, dev, stream):
             e1.record(stream)
             stream.synchronize()
             out[name] = host.numel() * 8 / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    if host2 is not None:
+        # both directions at once (what the pipelined e2e steps do): H2D host -> dev on one stream,
+        # D2H dev2 -> host2 on another, each timed by its own events
+        sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        stream.synchronize()
+        for _ in range(2):                       # the second pass is the timed one
+            with torch.cuda.stream(sa):
+                ev[0].record(sa)
+                dev.copy_(host, non_blocking=True)
+                ev[1].record(sa)
+            with torch.cuda.stream(sb):
+                ev[2].record(sb)
+                host2.copy_(dev2, non_blocking=True)
+                ev[3].record(sb)
+            sa.synchronize()
+            sb.synchronize()
+        out["h2d_both"] = host.numel() * 8 / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9
+        out["d2h_both"] = host.numel() * 8 / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9
     return out
 
 
@@ -291,11 +310,12 @@ def run_ours(args, rank, world, local_rank):
                 t = torch.tensor([te], device=red_dev, dtype=torch.float64)
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 te = float(t.item())
-            link = link_bandwidth(torch, fh, f, stream)
+            link = link_bandwidth(torch, fh, f, stream, xh, x)
             h2d_b = (1 if world == 1 else 2) * f.numel() * 8
             d2h_b = f.numel() * 8
-            # the copy bound of a fully pipelined step: the slower direction at the measured link speed
-            t_copy = max(h2d_b / (link["h2d"] * 1e9), d2h_b / (link["d2h"] * 1e9)) if link else None
+            # the copy bound of a fully pipelined step: the slower direction at the link speed measured
+            # with both directions busy (the steady state of the pipeline)
+            t_copy = max(h2d_b / (link["h2d_both"] * 1e9), d2h_b / (link["d2h_both"] * 1e9)) if link else None
             e2e = {"value": n_dofs * world / te, "unit": UNIT,
                    "h2d_bytes_per_step": h2d_b * world, "d2h_bytes_per_step": d2h_b * world, "note": note,
                    "link_GBps": link,
