@@ -1,3 +1,6 @@
+# One gpurun call that produces the round evidence under gpurun_out/ (copied to profiles/ afterwards):
+# GPU tests, ncu --set full per kernel (reports stay in /tmp on the box: gpurun_out/ is capped at 64 MiB),
+# plain bench + ncu launch list of the same command, final bench lines, smoke.
 mkdir -p gpurun_out
 H=$(python scripts/srchash.py)
 echo "srchash $H"
